@@ -1,0 +1,164 @@
+/*
+ * turbda_b200.h - C-ABI of the B200-native EnSF analysis step.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and PODs, no C++ or
+ * torch types.  The C++ API in include/turbda/ (turbda::analyze & co., the
+ * reference's own signatures) and the Python module
+ * paper_2407_12168_b200._core are thin hosts above it.
+ *
+ * Reference interfaces replaced (all paths under /root/reference/proj):
+ *   turbda_ensf_analyze   <- turbda::analyze          include/turbda/ensf.hpp:79-81,
+ *                                                    src/ensf.cpp:132-223
+ *                            (and its callers run_experiment src/osse.cpp:234-235,
+ *                             _core.ensf_analyze python/bindings.cpp:140-155)
+ *   turbda_relax_spread   <- turbda::relax_spread     include/turbda/ensf.hpp:85-86,
+ *                                                    src/ensf.cpp:225-258
+ *   turbda_score          <- turbda::prior_score / posterior_score
+ *                                                    include/turbda/ensf.hpp:52-70,
+ *                                                    src/ensf.cpp:68-82,96-106
+ *   turbda_diag           <- turbda::rmse / spread    include/turbda/ensemble.hpp:32-38,
+ *                                                    src/ensemble.cpp:18-43
+ *
+ * Error convention: every entry point returns a turbda_code and fills
+ * *status (when non-NULL).  The C++ host maps TURBDA_CONFIG -> ConfigError,
+ * TURBDA_DIMENSION -> DimensionError, TURBDA_DIVERGED ->
+ * SamplerDivergedError(diverged_t), TURBDA_DOMAIN -> std::domain_error, as the
+ * reference throws them (include/turbda/errors.hpp:9-57).
+ *
+ * There is no CPU fallback: without a CUDA device every compute entry point
+ * returns TURBDA_CUDA.
+ */
+#ifndef TURBDA_B200_H
+#define TURBDA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TURBDA_B200_ABI_VERSION 1
+
+typedef enum turbda_code {
+    TURBDA_OK = 0,
+    TURBDA_CONFIG = 1,     /* ConfigError                                  */
+    TURBDA_DIMENSION = 2,  /* DimensionError                               */
+    TURBDA_DIVERGED = 3,   /* SamplerDivergedError(pseudo_time)            */
+    TURBDA_DOMAIN = 4,     /* std::domain_error (score time outside [eps,1]) */
+    TURBDA_CUDA = 5,       /* no device / CUDA runtime failure             */
+    TURBDA_INTERNAL = 6
+} turbda_code;
+
+typedef enum turbda_precision {
+    TURBDA_FP32 = 0,  /* fast path: fp32 registers, MUFU ex2, packed FFMA2 */
+    TURBDA_FP64 = 1   /* faithful path: the reference's fp64 arithmetic    */
+} turbda_precision;
+
+/* flags */
+#define TURBDA_INPUTS_ON_DEVICE 0x1u /* every array pointer is a device pointer  */
+#define TURBDA_ASYNC 0x2u            /* device mode only: do not synchronize;     */
+                                     /* fetch the divergence verdict later with   */
+                                     /* turbda_ensf_check()                       */
+
+typedef struct turbda_status {
+    int32_t code;              /* turbda_code                                   */
+    int32_t diverged_particle; /* lowest particle index that went non-finite    */
+    int32_t diverged_step;     /* its first non-finite pseudo-time step         */
+    int32_t reserved;
+    double diverged_t;         /* pseudo-time of that step (t_ev)               */
+    char msg[256];
+} turbda_status;
+
+/*
+ * One EnSF analysis (turbda::analyze) on the coordinate window
+ * [k0, k0 + d_local) of a state of global dimension d_total.  A whole-state
+ * call has k0 = 0, d_local = d_total.  Because the reference's prior score is
+ * componentwise, every window reproduces exactly the coordinates a
+ * whole-state call would produce (the particle noise is keyed by the global
+ * coordinate), which is how the state dimension shards across GPUs.
+ */
+typedef struct turbda_ensf_params {
+    int64_t d_total;      /* global state dimension                              */
+    int64_t k0;           /* first global coordinate of the window               */
+    int64_t d_local;      /* coordinates in the window                           */
+    int64_t obs_dim;      /* entries of y / r_diag (/ obs_idx)                   */
+    int32_t n_members;    /* M: forecast members == analysis particles           */
+    int32_t n_steps;      /* EnsfConfig::n_steps (>= 10)                          */
+    int32_t minibatch_j;  /* EnsfConfig::minibatch_j (0 = all members)           */
+    int32_t obs_kind;     /* 0 identity (obs_dim == d_local), 1 index_selection  */
+    double eps;           /* EnsfConfig::eps in (0, 1)                            */
+    double damping_t;     /* EnsfConfig::damping_t: h(t) = damping_t - t          */
+    double relax_factor;  /* EnsfConfig::relax_factor in [0, 1]                   */
+    uint64_t seed;
+    uint64_t cycle;
+    int32_t precision;    /* turbda_precision                                    */
+    int32_t device;       /* first CUDA device; -1 = current device              */
+    int32_t device_count; /* >1 (host buffers only): split the window over       */
+                          /* devices device .. device + device_count - 1         */
+    uint32_t flags;       /* TURBDA_INPUTS_ON_DEVICE | TURBDA_ASYNC              */
+} turbda_ensf_params;
+
+/* Fills *p with the reference defaults (include/turbda/ensf.hpp:22-27):
+ * n_steps 100, eps 0.01, minibatch 0, damping_t 1, relax 1, fp32, device -1. */
+void turbda_ensf_params_init(turbda_ensf_params* p);
+
+/*
+ * forecast     [n_members][d_local] row-major fp64 (member-major, like the
+ *              reference's Ensemble::members and the Python (M, d) array)
+ * y, r_diag    [obs_dim] fp64
+ * obs_idx      [obs_dim] global state indices (index_selection); NULL for identity
+ * analysis_out [n_members][d_local] fp64
+ * stream       cudaStream_t to run on (device mode); NULL = per-device stream
+ */
+int turbda_ensf_analyze(const turbda_ensf_params* p, const double* forecast, const double* y,
+                        const double* r_diag, const int64_t* obs_idx, double* analysis_out,
+                        void* stream, turbda_status* status);
+
+/* Same analysis with the members kept as separate host rows (the
+ * reference's Ensemble::members layout): forecast_rows[j] and
+ * analysis_rows[j] point at d_local doubles each.  Host buffers only; saves
+ * the caller packing a contiguous [M][d] copy. */
+int turbda_ensf_analyze_rows(const turbda_ensf_params* p, const double* const* forecast_rows,
+                             const double* y, const double* r_diag, const int64_t* obs_idx,
+                             double* const* analysis_rows, turbda_status* status);
+
+/* After a TURBDA_ASYNC call and a synchronize of its stream: verdict of the
+ * most recent analysis on `device`. */
+int turbda_ensf_check(int device, const turbda_ensf_params* p, turbda_status* status);
+
+/* relax_spread on the device; host or device buffers per `flags`. */
+int turbda_relax_spread(const double* analysis, const double* forecast, int32_t n_members,
+                        int64_t d, double factor, double* out, int32_t device, uint32_t flags,
+                        void* stream, turbda_status* status);
+
+/*
+ * Componentwise prior score at pseudo-time t (prior_score), plus the damped
+ * likelihood when y != NULL (posterior_score), fp64, host buffers.
+ * batch: member indices or NULL (all members).
+ */
+int turbda_score(const double* z, int64_t d, double t, const double* forecast, int32_t n_members,
+                 const int32_t* batch, int32_t n_batch, double eps, const double* y,
+                 const double* r_diag, const int64_t* obs_idx, int64_t obs_dim, int32_t obs_kind,
+                 double damping_t, double* out, int32_t device, turbda_status* status);
+
+/* out[0] = sum_k (mean_k - truth_k)^2 (0 when truth == NULL),
+ * out[1] = sum_{j,k} (x_jk - mean_k)^2.  members / truth are host or device
+ * buffers per flags; out is always a host double[2]. */
+int turbda_diag(const double* members, int32_t n_members, int64_t d, const double* truth,
+                double* out, int32_t device, uint32_t flags, void* stream,
+                turbda_status* status);
+
+/* Number of CUDA devices (0 when none), library ABI version, and the name of
+ * the kernel family compiled in ("sm_100a"). */
+int turbda_device_count(void);
+int turbda_abi_version(void);
+const char* turbda_build_arch(void);
+
+/* Kernel launches issued by this process since load (evidence counter). */
+uint64_t turbda_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TURBDA_B200_H */

@@ -1,0 +1,213 @@
+"""ctypes binding of the C-ABI in ``include/turbda_b200.h``.
+
+This is the binding a maintainer of the reference would add on the Python
+side and the path ``bench.py`` uses for device-resident
+buffers (torch tensors, raw CUDA pointers).  It loads the in-tree
+``paper_2407_12168_b200/lib/libturbda_b200.so`` and raises if it is missing:
+there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libturbda_b200.so"
+
+OK, CONFIG, DIMENSION, DIVERGED, DOMAIN, CUDA, INTERNAL = range(7)
+FP32, FP64 = 0, 1
+INPUTS_ON_DEVICE = 0x1
+ASYNC = 0x2
+
+
+class EnsfParams(C.Structure):
+    _fields_ = [
+        ("d_total", C.c_int64), ("k0", C.c_int64), ("d_local", C.c_int64),
+        ("obs_dim", C.c_int64), ("n_members", C.c_int32), ("n_steps", C.c_int32),
+        ("minibatch_j", C.c_int32), ("obs_kind", C.c_int32), ("eps", C.c_double),
+        ("damping_t", C.c_double), ("relax_factor", C.c_double), ("seed", C.c_uint64),
+        ("cycle", C.c_uint64), ("precision", C.c_int32), ("device", C.c_int32),
+        ("device_count", C.c_int32), ("flags", C.c_uint32),
+    ]
+
+
+class Status(C.Structure):
+    _fields_ = [("code", C.c_int32), ("diverged_particle", C.c_int32),
+                ("diverged_step", C.c_int32), ("reserved", C.c_int32),
+                ("diverged_t", C.c_double), ("msg", C.c_char * 256)]
+
+
+class TurbdaError(RuntimeError):
+    def __init__(self, code: int, status: Status):
+        self.code = code
+        self.diverged_t = status.diverged_t
+        self.diverged_particle = status.diverged_particle
+        self.diverged_step = status.diverged_step
+        super().__init__(f"turbda_b200 code {code}: {status.msg.decode(errors='replace')}")
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(make -C paper_2407_12168_b200/csrc)")
+        L = C.CDLL(str(LIB_PATH))
+        vp, dp = C.c_void_p, C.POINTER(C.c_double)
+        L.turbda_ensf_params_init.argtypes = [C.POINTER(EnsfParams)]
+        L.turbda_ensf_params_init.restype = None
+        L.turbda_ensf_analyze.argtypes = [C.POINTER(EnsfParams), vp, vp, vp, vp, vp, vp,
+                                          C.POINTER(Status)]
+        L.turbda_ensf_analyze.restype = C.c_int
+        L.turbda_ensf_analyze_rows.argtypes = [C.POINTER(EnsfParams), vp, vp, vp, vp, vp,
+                                               C.POINTER(Status)]
+        L.turbda_ensf_analyze_rows.restype = C.c_int
+        L.turbda_ensf_check.argtypes = [C.c_int, C.POINTER(EnsfParams), C.POINTER(Status)]
+        L.turbda_ensf_check.restype = C.c_int
+        L.turbda_relax_spread.argtypes = [vp, vp, C.c_int32, C.c_int64, C.c_double, vp,
+                                          C.c_int32, C.c_uint32, vp, C.POINTER(Status)]
+        L.turbda_relax_spread.restype = C.c_int
+        L.turbda_score.argtypes = [vp, C.c_int64, C.c_double, vp, C.c_int32, vp, C.c_int32,
+                                   C.c_double, vp, vp, vp, C.c_int64, C.c_int32, C.c_double, vp,
+                                   C.c_int32, C.POINTER(Status)]
+        L.turbda_score.restype = C.c_int
+        L.turbda_diag.argtypes = [vp, C.c_int32, C.c_int64, vp, dp, C.c_int32, C.c_uint32, vp,
+                                  C.POINTER(Status)]
+        L.turbda_diag.restype = C.c_int
+        L.turbda_device_count.restype = C.c_int
+        L.turbda_abi_version.restype = C.c_int
+        L.turbda_build_arch.restype = C.c_char_p
+        L.turbda_launch_count.restype = C.c_uint64
+        _lib = L
+    return _lib
+
+
+def params(**kw) -> EnsfParams:
+    p = EnsfParams()
+    lib().turbda_ensf_params_init(C.byref(p))
+    for k, v in kw.items():
+        if not hasattr(p, k):
+            raise TypeError(f"unknown turbda_ensf_params field {k!r}")
+        setattr(p, k, v)
+    return p
+
+
+def _check(code: int, st: Status):
+    if code != OK:
+        raise TurbdaError(code, st)
+
+
+def _ptr(a) -> int | None:
+    """numpy array -> host address; torch tensor / int -> address; None -> NULL."""
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return a
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    raise TypeError(type(a))
+
+
+def analyze(p: EnsfParams, forecast, y, r_diag, obs_idx, out, stream: int | None = None):
+    """Raw C-ABI call.  With ``p.flags & INPUTS_ON_DEVICE`` every array is a
+    device buffer (torch CUDA tensor or int address) and ``stream`` a
+    cudaStream_t handle; otherwise numpy host arrays."""
+    st = Status()
+    code = lib().turbda_ensf_analyze(C.byref(p), _ptr(forecast), _ptr(y), _ptr(r_diag),
+                                     _ptr(obs_idx), _ptr(out), stream, C.byref(st))
+    _check(code, st)
+    return st
+
+
+def check(device: int, p: EnsfParams) -> Status:
+    st = Status()
+    _check(lib().turbda_ensf_check(device, C.byref(p), C.byref(st)), st)
+    return st
+
+
+def analyze_host(members, y, r=1.0, idx=None, *, n_steps=100, eps=0.01, minibatch_j=0,
+                 damping_t=1.0, relax_factor=1.0, seed=7, cycle=1, precision=FP32, device=-1,
+                 device_count=1, k0=0, d_total=None):
+    """numpy-in / numpy-out analysis over the window [k0, k0 + d) of a state
+    of dimension d_total (defaults to the whole state)."""
+    x = np.ascontiguousarray(members, dtype=np.float64)
+    m, d = x.shape
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    r = np.ascontiguousarray(np.broadcast_to(np.asarray(r, np.float64), y.shape))
+    ix = None if idx is None else np.ascontiguousarray(idx, dtype=np.int64)
+    p = params(d_total=d if d_total is None else d_total, k0=k0, d_local=d, obs_dim=y.size,
+               n_members=m, n_steps=n_steps, minibatch_j=minibatch_j,
+               obs_kind=0 if idx is None else 1, eps=eps, damping_t=damping_t,
+               relax_factor=relax_factor, seed=seed, cycle=cycle, precision=precision,
+               device=device, device_count=device_count)
+    out = np.empty_like(x)
+    analyze(p, x, y, r, ix, out)
+    return out
+
+
+def score(z, t, members, batch=None, eps=0.01, y=None, r=None, idx=None, damping_t=1.0,
+          device=-1):
+    z = np.ascontiguousarray(z, np.float64)
+    x = np.ascontiguousarray(members, np.float64)
+    b = None if batch is None else np.ascontiguousarray(batch, np.int32)
+    out = np.empty_like(z)
+    yy = rr = ii = None
+    nobs = 0
+    if y is not None:
+        yy = np.ascontiguousarray(y, np.float64)
+        rr = np.ascontiguousarray(np.broadcast_to(np.asarray(r, np.float64), yy.shape))
+        ii = None if idx is None else np.ascontiguousarray(idx, np.int64)
+        nobs = yy.size
+    st = Status()
+    code = lib().turbda_score(_ptr(z), z.size, t, _ptr(x), x.shape[0], _ptr(b),
+                              0 if b is None else b.size, eps, _ptr(yy), _ptr(rr), _ptr(ii),
+                              nobs, 0 if idx is None else 1, damping_t, _ptr(out), device,
+                              C.byref(st))
+    _check(code, st)
+    return out
+
+
+def relax_spread(analysis, forecast, factor, device=-1):
+    a = np.ascontiguousarray(analysis, np.float64)
+    f = np.ascontiguousarray(forecast, np.float64)
+    out = np.empty_like(a)
+    st = Status()
+    _check(lib().turbda_relax_spread(_ptr(a), _ptr(f), a.shape[0], a.shape[1], factor,
+                                     _ptr(out), device, 0, None, C.byref(st)), st)
+    return out
+
+
+def diag(members, truth=None, device=-1):
+    x = np.ascontiguousarray(members, np.float64)
+    t = None if truth is None else np.ascontiguousarray(truth, np.float64)
+    out = (C.c_double * 2)()
+    st = Status()
+    _check(lib().turbda_diag(_ptr(x), x.shape[0], x.shape[1], _ptr(t), out, device, 0, None,
+                             C.byref(st)), st)
+    return float(out[0]), float(out[1])
+
+
+def device_count() -> int:
+    return int(lib().turbda_device_count())
+
+
+def launch_count() -> int:
+    return int(lib().turbda_launch_count())
+
+
+def exported_symbols() -> list[str]:
+    """Symbols include/turbda_b200.h declares (checked by the CPU tests)."""
+    hdr = Path(__file__).resolve().parents[1] / "include" / "turbda_b200.h"
+    import re
+    return sorted(set(re.findall(r"\b(turbda_[a-z0-9_]+)\s*\(", hdr.read_text())))
+
+
+if os.environ.get("TURBDA_B200_EAGER_LOAD"):
+    lib()

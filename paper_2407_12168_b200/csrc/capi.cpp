@@ -1,0 +1,702 @@
+// C-ABI implementation (include/turbda_b200.h): validation, host-side
+// precomputation of the pseudo-time grid and minibatch tables, per-device
+// workspaces, H2D/D2H staging and the kernel sequence
+//   obs_prep -> ensf_{f32,f64} (all pseudo-time steps fused) -> relax.
+#include "turbda_b200.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "ensf_device.h"
+#include "host_rng.h"
+
+using namespace tb200;
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+int fail(turbda_status* st, int code, const std::string& msg) {
+    if (st) {
+        st->code = code;
+        std::snprintf(st->msg, sizeof(st->msg), "%s", msg.c_str());
+    }
+    return code;
+}
+
+int cuda_fail(turbda_status* st, cudaError_t e, const char* where) {
+    return fail(st, TURBDA_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define TB_CUDA(call)                                          \
+    do {                                                       \
+        cudaError_t e_ = (call);                               \
+        if (e_ != cudaSuccess) return cuda_fail(st, e_, #call); \
+    } while (0)
+
+// Device buffer that only grows.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(bytes, 256);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+// Per-device workspace, serialised by `mu` (calls are reentrant across devices).
+struct Workspace {
+    std::mutex mu;
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    DevBuf x, z, ab, steps, batches, status, out, y, r, idx;
+    unsigned long long* status_host = nullptr;  // pinned
+    // cached step table / batch table keys
+    std::vector<unsigned char> steps_key, batch_key;
+    // last analysis (for turbda_ensf_check)
+    int last_m = 0, last_steps = 0;
+    double last_eps = 0.0;
+};
+
+std::mutex g_ws_mu;
+std::vector<std::unique_ptr<Workspace>> g_ws;
+
+Workspace* workspace(int device) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    if (device < 0) return nullptr;
+    if (size_t(device) >= g_ws.size()) g_ws.resize(size_t(device) + 1);
+    if (!g_ws[size_t(device)]) {
+        g_ws[size_t(device)] = std::make_unique<Workspace>();
+        g_ws[size_t(device)]->device = device;
+    }
+    return g_ws[size_t(device)].get();
+}
+
+int ws_init(Workspace* w, turbda_status* st) {
+    if (!w->stream) {
+        TB_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
+        TB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->status_host), 64));
+    }
+    return TURBDA_OK;
+}
+
+// proj/src/ensf.cpp:149,183-190 and proj/include/turbda/ensf.hpp:15-20
+struct StepTimes {
+    double t_ev, alpha, beta2, b, s2, damp, sig, dt;
+};
+
+std::vector<StepTimes> step_grid(int n_steps, double eps, double damping_t) {
+    std::vector<StepTimes> g(static_cast<size_t>(n_steps));
+    const double dt = (1.0 - eps) / n_steps;
+    for (int s = 0; s < n_steps; ++s) {
+        const double t_hi = 1.0 - s * dt;
+        const double t = std::max(t_hi - dt, eps);
+        StepTimes& q = g[size_t(s)];
+        q.t_ev = t;
+        q.alpha = 1.0 - t;
+        q.beta2 = t;
+        q.b = -1.0 / (1.0 - t);
+        q.s2 = 1.0 + 2.0 * t / (1.0 - t);
+        q.damp = damping_t - t;
+        q.sig = std::sqrt(q.s2 * dt);
+        q.dt = dt;
+    }
+    return g;
+}
+
+double step_time(int step, int n_steps, double eps) {
+    const double dt = (1.0 - eps) / n_steps;
+    return std::max(1.0 - step * dt - dt, eps);
+}
+
+// proj/src/ensf.cpp:151-168: partial Fisher-Yates per step
+std::vector<int32_t> batch_table(uint64_t seed, uint64_t cycle, int m, int j, int n_steps) {
+    std::vector<int32_t> t(size_t(n_steps) * size_t(j));
+    std::vector<int32_t> pool(static_cast<size_t>(m));
+    for (int s = 0; s < n_steps; ++s) {
+        HostStream rs(seed, kUseEnsfBatch, (cycle << 20) + uint64_t(s));
+        for (int q = 0; q < m; ++q) pool[size_t(q)] = q;
+        for (int k = 0; k < j; ++k) {
+            const int r = k + int(rs.next_u64() % uint64_t(m - k));
+            std::swap(pool[size_t(k)], pool[size_t(r)]);
+        }
+        std::copy(pool.begin(), pool.begin() + j, t.begin() + size_t(s) * size_t(j));
+    }
+    return t;
+}
+
+template <class T>
+std::vector<unsigned char> key_bytes(const T& v) {
+    std::vector<unsigned char> k(sizeof(T));
+    std::memcpy(k.data(), &v, sizeof(T));
+    return k;
+}
+
+int validate(const turbda_ensf_params* p, turbda_status* st) {
+    if (!p) return fail(st, TURBDA_CONFIG, "ensf: null params");
+    // Ensemble::validate(false), include/turbda/ensemble.hpp:23-33
+    if (p->n_members < 1) return fail(st, TURBDA_DIMENSION, "ensemble: empty");
+    if (p->d_local < 0 || p->k0 < 0 || p->d_total < p->k0 + p->d_local)
+        return fail(st, TURBDA_DIMENSION, "analyze: window outside the state");
+    // Observation::validate length check, include/turbda/observation.hpp:49-55
+    if (p->obs_kind == 0 && p->obs_dim != p->d_local)
+        return fail(st, TURBDA_DIMENSION, "observation: length mismatch");
+    if (p->obs_kind != 0 && p->obs_kind != 1)
+        return fail(st, TURBDA_CONFIG, "observation: unsupported operator kind");
+    if (p->obs_dim < 0) return fail(st, TURBDA_DIMENSION, "observation: length mismatch");
+    // EnsfConfig::validate, include/turbda/ensf.hpp:29-37
+    if (!(p->eps > 0.0 && p->eps < 1.0)) return fail(st, TURBDA_CONFIG, "ensf: eps must lie in (0, 1)");
+    if (p->n_steps < 10) return fail(st, TURBDA_CONFIG, "ensf: n_steps >= 10");
+    if (p->minibatch_j < 0) return fail(st, TURBDA_CONFIG, "ensf: minibatch_j >= 0");
+    if (p->relax_factor < 0.0 || p->relax_factor > 1.0)
+        return fail(st, TURBDA_CONFIG, "ensf: relax_factor in [0, 1]");
+    if (p->precision != TURBDA_FP32 && p->precision != TURBDA_FP64)
+        return fail(st, TURBDA_CONFIG, "ensf: precision must be fp32 (0) or fp64 (1)");
+    if (p->n_members > (1 << 24)) return fail(st, TURBDA_CONFIG, "ensf: too many members");
+    return TURBDA_OK;
+}
+
+int validate_host_obs(const turbda_ensf_params* p, const double* r, const int64_t* idx,
+                      turbda_status* st) {
+    for (int64_t q = 0; q < p->obs_dim; ++q)
+        if (!(r[q] > 0.0)) return fail(st, TURBDA_CONFIG, "observation: r_diag > 0");
+    if (p->obs_kind == 1)
+        for (int64_t q = 0; q < p->obs_dim; ++q)
+            if (idx[q] < 0 || idx[q] >= p->d_total)
+                return fail(st, TURBDA_DIMENSION, "observation: index outside the state");
+    return TURBDA_OK;
+}
+
+int diverged(const turbda_ensf_params* p, unsigned long long word, turbda_status* st) {
+    if (word == kNoDivergence) return TURBDA_OK;
+    const int particle = int(word >> 32);
+    const int step = int(word & 0xffffffffu);
+    const double t = step_time(step, p->n_steps, p->eps);
+    if (st) {
+        st->diverged_particle = particle;
+        st->diverged_step = step;
+        st->diverged_t = t;
+    }
+    // message text of SamplerDivergedError, include/turbda/errors.hpp:36-42
+    return fail(st, TURBDA_DIVERGED, "reverse SDE diverged at pseudo-time t=" + std::to_string(t));
+}
+
+// Uploads the per-step coefficient table (cached by its defining parameters).
+int upload_steps(Workspace* w, const turbda_ensf_params* p, cudaStream_t s, turbda_status* st) {
+    struct Key {
+        int32_t n_steps, precision;
+        double eps, damping_t;
+    } key{p->n_steps, p->precision, p->eps, p->damping_t};
+    std::vector<unsigned char> kb = key_bytes(key);
+    if (kb == w->steps_key && w->steps.p) return TURBDA_OK;
+    const std::vector<StepTimes> g = step_grid(p->n_steps, p->eps, p->damping_t);
+    if (p->precision == TURBDA_FP32) {
+        std::vector<StepF32> h(g.size());
+        const double log2e = 1.4426950408889634;
+        for (size_t s2 = 0; s2 < g.size(); ++s2) {
+            const StepTimes& q = g[s2];
+            StepF32& o = h[s2];
+            o.na = float(-q.alpha);
+            o.cl = float(log2e / (2.0 * q.beta2));
+            o.kp = float(-q.s2 * q.dt / q.beta2);
+            o.kl = float(q.s2 * q.dt * q.damp);
+            o.nbdt = float(-q.b * q.dt);
+            o.sig = float(q.sig);
+            o.pad0 = o.pad1 = 0.f;
+        }
+        TB_CUDA(w->steps.reserve(sizeof(StepF32) * h.size()));
+        TB_CUDA(cudaMemcpyAsync(w->steps.p, h.data(), sizeof(StepF32) * h.size(),
+                                cudaMemcpyHostToDevice, s));
+        TB_CUDA(cudaStreamSynchronize(s));
+    } else {
+        std::vector<StepF64> h(g.size());
+        for (size_t s2 = 0; s2 < g.size(); ++s2) {
+            const StepTimes& q = g[s2];
+            h[s2] = StepF64{q.alpha, q.beta2, 1.0 / (2.0 * q.beta2), q.b, q.s2, q.damp, q.sig, q.dt};
+        }
+        TB_CUDA(w->steps.reserve(sizeof(StepF64) * h.size()));
+        TB_CUDA(cudaMemcpyAsync(w->steps.p, h.data(), sizeof(StepF64) * h.size(),
+                                cudaMemcpyHostToDevice, s));
+        TB_CUDA(cudaStreamSynchronize(s));
+    }
+    w->steps_key = kb;
+    return TURBDA_OK;
+}
+
+int upload_batches(Workspace* w, const turbda_ensf_params* p, int j_batch, cudaStream_t s,
+                   turbda_status* st) {
+    struct Key {
+        uint64_t seed, cycle;
+        int32_t m, j, n_steps;
+    } key{p->seed, p->cycle, p->n_members, j_batch, p->n_steps};
+    std::vector<unsigned char> kb = key_bytes(key);
+    if (kb == w->batch_key && w->batches.p) return TURBDA_OK;
+    const std::vector<int32_t> t = batch_table(p->seed, p->cycle, p->n_members, j_batch, p->n_steps);
+    TB_CUDA(w->batches.reserve(sizeof(int32_t) * t.size()));
+    TB_CUDA(cudaMemcpyAsync(w->batches.p, t.data(), sizeof(int32_t) * t.size(),
+                            cudaMemcpyHostToDevice, s));
+    TB_CUDA(cudaStreamSynchronize(s));
+    w->batch_key = kb;
+    return TURBDA_OK;
+}
+
+struct Window {
+    int64_t k0_local;  // offset of this device's slice inside the call's window
+    int64_t dl;        // coordinates in this slice
+};
+
+// Runs one analysis slice on one device.  Host mode: `forecast`/`out` are the
+// call's host arrays with row pitch p->d_local; the slice starts at column
+// win.k0_local.  Device mode: pointers are device pointers of the full window.
+int run_slice(const turbda_ensf_params* p, const Window& win, int device, const double* forecast,
+              const double* const* frows, const double* y, const double* r, const int64_t* idx,
+              double* out, double* const* orows, cudaStream_t user_stream, turbda_status* st) {
+    const bool on_dev = (p->flags & TURBDA_INPUTS_ON_DEVICE) != 0;
+    TB_CUDA(cudaSetDevice(device));
+    Workspace* w = workspace(device);
+    std::lock_guard<std::mutex> lk(w->mu);
+    if (int rc = ws_init(w, st)) return rc;
+    cudaStream_t s = user_stream ? user_stream : w->stream;
+
+    const int m = p->n_members;
+    const int64_t dl = win.dl;
+    const size_t md = size_t(m) * size_t(dl);
+    const int j_batch = (p->minibatch_j == 0 || p->minibatch_j >= m) ? m : p->minibatch_j;
+    const bool fp32 = p->precision == TURBDA_FP32;
+
+    if (int rc = upload_steps(w, p, s, st)) return rc;
+    if (j_batch != m)
+        if (int rc = upload_batches(w, p, j_batch, s, st)) return rc;
+
+    const double* dx;
+    const double *dy, *dr;
+    const int64_t* didx = nullptr;
+    double* dout;
+    int64_t obs_n = p->obs_dim;
+    if (on_dev) {
+        dx = forecast;
+        dy = y;
+        dr = r;
+        didx = idx;
+        dout = out;
+    } else {
+        TB_CUDA(w->x.reserve(sizeof(double) * md));
+        TB_CUDA(w->out.reserve(sizeof(double) * md));
+        // forecast slice [m][k0_local : k0_local + dl] of the host [m][d_local]
+        // array, or of the member rows when the caller keeps them apart
+        if (dl > 0 && m > 0) {
+            if (frows) {
+                for (int j = 0; j < m; ++j)
+                    TB_CUDA(cudaMemcpyAsync(w->x.as<double>() + size_t(j) * size_t(dl),
+                                            frows[j] + win.k0_local, sizeof(double) * size_t(dl),
+                                            cudaMemcpyHostToDevice, s));
+            } else {
+                TB_CUDA(cudaMemcpy2DAsync(w->x.p, sizeof(double) * size_t(dl),
+                                          forecast + win.k0_local,
+                                          sizeof(double) * size_t(p->d_local),
+                                          sizeof(double) * size_t(dl), size_t(m),
+                                          cudaMemcpyHostToDevice, s));
+            }
+        }
+        if (p->obs_kind == 0) {
+            obs_n = dl;
+            TB_CUDA(w->y.reserve(sizeof(double) * size_t(std::max<int64_t>(obs_n, 1))));
+            TB_CUDA(w->r.reserve(sizeof(double) * size_t(std::max<int64_t>(obs_n, 1))));
+            if (obs_n > 0) {
+                TB_CUDA(cudaMemcpyAsync(w->y.p, y + win.k0_local, sizeof(double) * size_t(obs_n),
+                                        cudaMemcpyHostToDevice, s));
+                TB_CUDA(cudaMemcpyAsync(w->r.p, r + win.k0_local, sizeof(double) * size_t(obs_n),
+                                        cudaMemcpyHostToDevice, s));
+            }
+        } else {
+            const size_t nb = size_t(std::max<int64_t>(obs_n, 1));
+            TB_CUDA(w->y.reserve(sizeof(double) * nb));
+            TB_CUDA(w->r.reserve(sizeof(double) * nb));
+            TB_CUDA(w->idx.reserve(sizeof(int64_t) * nb));
+            if (obs_n > 0) {
+                TB_CUDA(cudaMemcpyAsync(w->y.p, y, sizeof(double) * size_t(obs_n),
+                                        cudaMemcpyHostToDevice, s));
+                TB_CUDA(cudaMemcpyAsync(w->r.p, r, sizeof(double) * size_t(obs_n),
+                                        cudaMemcpyHostToDevice, s));
+                TB_CUDA(cudaMemcpyAsync(w->idx.p, idx, sizeof(int64_t) * size_t(obs_n),
+                                        cudaMemcpyHostToDevice, s));
+            }
+            didx = w->idx.as<int64_t>();
+        }
+        dx = w->x.as<double>();
+        dy = w->y.as<double>();
+        dr = w->r.as<double>();
+        dout = w->out.as<double>();
+    }
+
+    TB_CUDA(w->z.reserve((fp32 ? sizeof(float) : sizeof(double)) * std::max<size_t>(md, 1)));
+    TB_CUDA(w->ab.reserve(sizeof(double2) * size_t(std::max<int64_t>(dl, 1))));
+    TB_CUDA(w->status.reserve(64));
+    TB_CUDA(cudaMemsetAsync(w->status.p, 0xff, sizeof(unsigned long long), s));
+
+    const int64_t k0_global = p->k0 + win.k0_local;
+    TB_CUDA(launch_obs_prep(dy, dr, didx, obs_n, p->obs_kind, k0_global, dl, w->ab.as<double2>(), s));
+    g_launches += (p->obs_kind == 0) ? 1 : 2;
+
+    KernelArgs a{};
+    a.d_total = p->d_total;
+    a.k0 = k0_global;
+    a.dl = dl;
+    a.m = m;
+    a.n_steps = p->n_steps;
+    a.j_batch = j_batch;
+    a.minibatch = j_batch != m;
+    const uint64_t key = stream_key(p->seed, kUseEnsfParticles);
+    a.key0 = uint32_t(key);
+    a.key1 = uint32_t(key >> 32);
+    a.cycle_lo = uint32_t(p->cycle);  // entity = (cycle << 32) | i
+
+    unsigned long long* dstatus = w->status.as<unsigned long long>();
+    if (fp32) {
+        TB_CUDA(launch_ensf_f32(a, dx, w->ab.as<double2>(), w->steps.as<StepF32>(),
+                                w->batches.as<int32_t>(), w->z.as<float>(), dstatus, s));
+        TB_CUDA(launch_relax_f32(w->z.as<float>(), dx, m, dl, p->relax_factor, dout, s));
+    } else {
+        TB_CUDA(launch_ensf_f64(a, dx, w->ab.as<double2>(), w->steps.as<StepF64>(),
+                                w->batches.as<int32_t>(), w->z.as<double>(), dstatus, s));
+        TB_CUDA(launch_relax_f64(w->z.as<double>(), dx, m, dl, p->relax_factor, dout, s));
+    }
+    g_launches += 2;
+    w->last_m = m;
+    w->last_steps = p->n_steps;
+    w->last_eps = p->eps;
+
+    if (on_dev && (p->flags & TURBDA_ASYNC)) return TURBDA_OK;
+
+    TB_CUDA(cudaMemcpyAsync(w->status_host, dstatus, sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s));
+    if (!on_dev && dl > 0 && m > 0) {
+        if (orows) {
+            for (int j = 0; j < m; ++j)
+                TB_CUDA(cudaMemcpyAsync(orows[j] + win.k0_local, dout + size_t(j) * size_t(dl),
+                                        sizeof(double) * size_t(dl), cudaMemcpyDeviceToHost, s));
+        } else {
+            TB_CUDA(cudaMemcpy2DAsync(out + win.k0_local, sizeof(double) * size_t(p->d_local),
+                                      dout, sizeof(double) * size_t(dl),
+                                      sizeof(double) * size_t(dl), size_t(m),
+                                      cudaMemcpyDeviceToHost, s));
+        }
+    }
+    TB_CUDA(cudaStreamSynchronize(s));
+    return diverged(p, *w->status_host, st);
+}
+
+int resolve_device(int requested, turbda_status* st, int* out) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fail(st, TURBDA_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    int dev = requested;
+    if (dev < 0) TB_CUDA(cudaGetDevice(&dev));
+    if (dev >= n) return fail(st, TURBDA_CUDA, "device ordinal out of range");
+    *out = dev;
+    return TURBDA_OK;
+}
+
+void clear(turbda_status* st) {
+    if (!st) return;
+    std::memset(st, 0, sizeof(*st));
+    st->diverged_particle = -1;
+    st->diverged_step = -1;
+    st->diverged_t = std::nan("");
+}
+
+}  // namespace
+
+extern "C" {
+
+void turbda_ensf_params_init(turbda_ensf_params* p) {
+    std::memset(p, 0, sizeof(*p));
+    p->n_steps = 100;
+    p->eps = 0.01;
+    p->minibatch_j = 0;
+    p->damping_t = 1.0;
+    p->relax_factor = 1.0;
+    p->seed = 7;
+    p->cycle = 1;
+    p->precision = TURBDA_FP32;
+    p->device = -1;
+    p->device_count = 1;
+}
+
+}  // extern "C"
+
+namespace {
+
+int analyze_impl(const turbda_ensf_params* p, const double* forecast, const double* const* frows,
+                 const double* y, const double* r_diag, const int64_t* obs_idx,
+                 double* analysis_out, double* const* orows, void* stream, turbda_status* st) {
+    clear(st);
+    if (int rc = validate(p, st)) return rc;
+    const bool on_dev = (p->flags & TURBDA_INPUTS_ON_DEVICE) != 0;
+    if (!on_dev) {
+        if (int rc = validate_host_obs(p, r_diag, obs_idx, st)) return rc;
+    }
+    int dev0 = 0;
+    if (int rc = resolve_device(p->device, st, &dev0)) return rc;
+    int ndev = std::max(1, p->device_count);
+    int avail = 0;
+    cudaGetDeviceCount(&avail);
+    if (dev0 + ndev > avail) return fail(st, TURBDA_CUDA, "device_count exceeds visible devices");
+    if (on_dev && ndev > 1)
+        return fail(st, TURBDA_CONFIG, "device_count > 1 needs host buffers");
+    if (p->d_local == 0) return TURBDA_OK;
+
+    if (ndev == 1)
+        return run_slice(p, Window{0, p->d_local}, dev0, forecast, frows, y, r_diag, obs_idx,
+                         analysis_out, orows, static_cast<cudaStream_t>(stream), st);
+
+    // state-dimension sharding: contiguous slices aligned to the 64-coordinate tile
+    std::vector<Window> wins;
+    const int64_t tiles = (p->d_local + 63) / 64;
+    int64_t start = 0;
+    for (int g = 0; g < ndev; ++g) {
+        const int64_t t_end = tiles * (g + 1) / ndev;
+        const int64_t end = std::min<int64_t>(p->d_local, t_end * 64);
+        wins.push_back(Window{start, end - start});
+        start = end;
+    }
+    std::vector<turbda_status> sts(static_cast<size_t>(ndev));
+    std::vector<int> rcs(static_cast<size_t>(ndev), 0);
+    std::vector<std::thread> th;
+    for (int g = 0; g < ndev; ++g) {
+        clear(&sts[size_t(g)]);
+        th.emplace_back([&, g] {
+            rcs[size_t(g)] = run_slice(p, wins[size_t(g)], dev0 + g, forecast, frows, y, r_diag,
+                                       obs_idx, analysis_out, orows, nullptr, &sts[size_t(g)]);
+        });
+    }
+    for (auto& t : th) t.join();
+    // non-divergence failures first (first device wins), then the lowest
+    // diverging particle / earliest step across shards
+    for (int g = 0; g < ndev; ++g)
+        if (rcs[size_t(g)] != TURBDA_OK && rcs[size_t(g)] != TURBDA_DIVERGED) {
+            if (st) *st = sts[size_t(g)];
+            return rcs[size_t(g)];
+        }
+    int best = -1;
+    for (int g = 0; g < ndev; ++g) {
+        if (rcs[size_t(g)] != TURBDA_DIVERGED) continue;
+        const turbda_status& q = sts[size_t(g)];
+        if (best < 0 || q.diverged_particle < sts[size_t(best)].diverged_particle ||
+            (q.diverged_particle == sts[size_t(best)].diverged_particle &&
+             q.diverged_step < sts[size_t(best)].diverged_step))
+            best = g;
+    }
+    if (best >= 0) {
+        if (st) *st = sts[size_t(best)];
+        return TURBDA_DIVERGED;
+    }
+    return TURBDA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int turbda_ensf_analyze(const turbda_ensf_params* p, const double* forecast, const double* y,
+                        const double* r_diag, const int64_t* obs_idx, double* analysis_out,
+                        void* stream, turbda_status* st) {
+    return analyze_impl(p, forecast, nullptr, y, r_diag, obs_idx, analysis_out, nullptr, stream,
+                        st);
+}
+
+int turbda_ensf_analyze_rows(const turbda_ensf_params* p, const double* const* forecast_rows,
+                             const double* y, const double* r_diag, const int64_t* obs_idx,
+                             double* const* analysis_rows, turbda_status* st) {
+    if (p && (p->flags & TURBDA_INPUTS_ON_DEVICE)) {
+        clear(st);
+        return fail(st, TURBDA_CONFIG, "turbda_ensf_analyze_rows takes host rows");
+    }
+    return analyze_impl(p, nullptr, forecast_rows, y, r_diag, obs_idx, nullptr, analysis_rows,
+                        nullptr, st);
+}
+
+int turbda_ensf_check(int device, const turbda_ensf_params* p, turbda_status* st) {
+    clear(st);
+    int dev = 0;
+    if (int rc = resolve_device(device, st, &dev)) return rc;
+    TB_CUDA(cudaSetDevice(dev));
+    Workspace* w = workspace(dev);
+    std::lock_guard<std::mutex> lk(w->mu);
+    if (!w->status.p) return TURBDA_OK;
+    unsigned long long word = kNoDivergence;
+    TB_CUDA(cudaMemcpy(&word, w->status.p, sizeof(word), cudaMemcpyDeviceToHost));
+    return diverged(p, word, st);
+}
+
+int turbda_relax_spread(const double* analysis, const double* forecast, int32_t m, int64_t d,
+                        double factor, double* out, int32_t device, uint32_t flags, void* stream,
+                        turbda_status* st) {
+    clear(st);
+    if (m < 1) return fail(st, TURBDA_DIMENSION, "ensemble: empty");
+    int dev = 0;
+    if (int rc = resolve_device(device, st, &dev)) return rc;
+    TB_CUDA(cudaSetDevice(dev));
+    Workspace* w = workspace(dev);
+    std::lock_guard<std::mutex> lk(w->mu);
+    if (int rc = ws_init(w, st)) return rc;
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : w->stream;
+    const size_t md = size_t(m) * size_t(d);
+    if (flags & TURBDA_INPUTS_ON_DEVICE) {
+        TB_CUDA(launch_relax_f64(analysis, forecast, m, d, factor, out, s));
+        ++g_launches;
+        TB_CUDA(cudaStreamSynchronize(s));
+        return TURBDA_OK;
+    }
+    TB_CUDA(w->x.reserve(sizeof(double) * std::max<size_t>(md, 1)));
+    TB_CUDA(w->z.reserve(sizeof(double) * std::max<size_t>(md, 1)));
+    TB_CUDA(w->out.reserve(sizeof(double) * std::max<size_t>(md, 1)));
+    TB_CUDA(cudaMemcpyAsync(w->z.p, analysis, sizeof(double) * md, cudaMemcpyHostToDevice, s));
+    TB_CUDA(cudaMemcpyAsync(w->x.p, forecast, sizeof(double) * md, cudaMemcpyHostToDevice, s));
+    TB_CUDA(launch_relax_f64(w->z.as<double>(), w->x.as<double>(), m, d, factor,
+                             w->out.as<double>(), s));
+    ++g_launches;
+    TB_CUDA(cudaMemcpyAsync(out, w->out.p, sizeof(double) * md, cudaMemcpyDeviceToHost, s));
+    TB_CUDA(cudaStreamSynchronize(s));
+    return TURBDA_OK;
+}
+
+int turbda_score(const double* z, int64_t d, double t, const double* forecast, int32_t m,
+                 const int32_t* batch, int32_t n_batch, double eps, const double* y,
+                 const double* r_diag, const int64_t* obs_idx, int64_t obs_dim, int32_t obs_kind,
+                 double damping_t, double* out, int32_t device, turbda_status* st) {
+    clear(st);
+    // check_score_time, proj/src/ensf.cpp:15-19
+    if (t < eps) return fail(st, TURBDA_DOMAIN, "prior_score: t below eps (beta -> 0)");
+    if (t > 1.0) return fail(st, TURBDA_DOMAIN, "prior_score: t > 1");
+    if (m < 1) return fail(st, TURBDA_DIMENSION, "ensemble: empty");
+    const int nb = (batch && n_batch > 0) ? n_batch : m;
+    if (batch)
+        for (int q = 0; q < n_batch; ++q)
+            if (batch[q] < 0 || batch[q] >= m)
+                return fail(st, TURBDA_DIMENSION, "prior_score: batch index out of range");
+    if (y) {
+        if ((obs_kind == 0 && obs_dim != d) || obs_dim < 0)
+            return fail(st, TURBDA_DIMENSION, "likelihood_score: dimension mismatch");
+        for (int64_t q = 0; q < obs_dim; ++q)
+            if (!(r_diag[q] > 0.0)) return fail(st, TURBDA_CONFIG, "observation: r_diag > 0");
+        if (obs_kind == 1)
+            for (int64_t q = 0; q < obs_dim; ++q)
+                if (obs_idx[q] < 0 || obs_idx[q] >= d)
+                    return fail(st, TURBDA_DIMENSION, "observation: index outside the state");
+    }
+    int dev = 0;
+    if (int rc = resolve_device(device, st, &dev)) return rc;
+    TB_CUDA(cudaSetDevice(dev));
+    Workspace* w = workspace(dev);
+    std::lock_guard<std::mutex> lk(w->mu);
+    if (int rc = ws_init(w, st)) return rc;
+    cudaStream_t s = w->stream;
+    const size_t md = size_t(m) * size_t(d);
+    const size_t d1 = size_t(std::max<int64_t>(d, 1));
+    TB_CUDA(w->x.reserve(sizeof(double) * std::max<size_t>(md, 1)));
+    TB_CUDA(w->z.reserve(sizeof(double) * d1));
+    TB_CUDA(w->out.reserve(sizeof(double) * d1));
+    TB_CUDA(w->batches.reserve(sizeof(int32_t) * size_t(std::max(nb, 1))));
+    w->batch_key.clear();
+    TB_CUDA(cudaMemcpyAsync(w->x.p, forecast, sizeof(double) * md, cudaMemcpyHostToDevice, s));
+    TB_CUDA(cudaMemcpyAsync(w->z.p, z, sizeof(double) * size_t(d), cudaMemcpyHostToDevice, s));
+    if (batch)
+        TB_CUDA(cudaMemcpyAsync(w->batches.p, batch, sizeof(int32_t) * size_t(nb),
+                                cudaMemcpyHostToDevice, s));
+    const double2* dab = nullptr;
+    double damp = 0.0;
+    if (y) {
+        const size_t nb2 = size_t(std::max<int64_t>(obs_dim, 1));
+        TB_CUDA(w->y.reserve(sizeof(double) * nb2));
+        TB_CUDA(w->r.reserve(sizeof(double) * nb2));
+        TB_CUDA(w->idx.reserve(sizeof(int64_t) * nb2));
+        TB_CUDA(w->ab.reserve(sizeof(double2) * d1));
+        if (obs_dim > 0) {
+            TB_CUDA(cudaMemcpyAsync(w->y.p, y, sizeof(double) * size_t(obs_dim), cudaMemcpyHostToDevice, s));
+            TB_CUDA(cudaMemcpyAsync(w->r.p, r_diag, sizeof(double) * size_t(obs_dim), cudaMemcpyHostToDevice, s));
+            if (obs_kind == 1)
+                TB_CUDA(cudaMemcpyAsync(w->idx.p, obs_idx, sizeof(int64_t) * size_t(obs_dim),
+                                        cudaMemcpyHostToDevice, s));
+        }
+        TB_CUDA(launch_obs_prep(w->y.as<double>(), w->r.as<double>(), w->idx.as<int64_t>(), obs_dim,
+                                obs_kind, 0, d, w->ab.as<double2>(), s));
+        ++g_launches;
+        dab = w->ab.as<double2>();
+        damp = damping_t - t;
+    }
+    // NoiseSchedule::alpha / beta2, include/turbda/ensf.hpp:15-20
+    TB_CUDA(launch_score_f64(w->z.as<double>(), w->x.as<double>(), m, d,
+                             batch ? w->batches.as<int32_t>() : nullptr, nb, 1.0 - t, t, dab, damp,
+                             w->out.as<double>(), s));
+    ++g_launches;
+    TB_CUDA(cudaMemcpyAsync(out, w->out.p, sizeof(double) * size_t(d), cudaMemcpyDeviceToHost, s));
+    TB_CUDA(cudaStreamSynchronize(s));
+    return TURBDA_OK;
+}
+
+int turbda_diag(const double* members, int32_t m, int64_t d, const double* truth, double* out,
+                int32_t device, uint32_t flags, void* stream, turbda_status* st) {
+    clear(st);
+    if (m < 1) return fail(st, TURBDA_DIMENSION, "ensemble: empty");
+    int dev = 0;
+    if (int rc = resolve_device(device, st, &dev)) return rc;
+    TB_CUDA(cudaSetDevice(dev));
+    Workspace* w = workspace(dev);
+    std::lock_guard<std::mutex> lk(w->mu);
+    if (int rc = ws_init(w, st)) return rc;
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : w->stream;
+    TB_CUDA(w->status.reserve(64));
+    double* dsum = reinterpret_cast<double*>(w->status.as<unsigned char>() + 16);
+    const size_t md = size_t(m) * size_t(d);
+    const double* dx = members;
+    const double* dt = truth;
+    if (!(flags & TURBDA_INPUTS_ON_DEVICE)) {
+        TB_CUDA(w->x.reserve(sizeof(double) * std::max<size_t>(md, 1)));
+        TB_CUDA(cudaMemcpyAsync(w->x.p, members, sizeof(double) * md, cudaMemcpyHostToDevice, s));
+        dx = w->x.as<double>();
+        if (truth) {
+            TB_CUDA(w->y.reserve(sizeof(double) * size_t(std::max<int64_t>(d, 1))));
+            TB_CUDA(cudaMemcpyAsync(w->y.p, truth, sizeof(double) * size_t(d), cudaMemcpyHostToDevice, s));
+            dt = w->y.as<double>();
+        }
+    }
+    TB_CUDA(launch_diag(dx, m, d, dt, dsum, s));
+    ++g_launches;
+    TB_CUDA(cudaMemcpyAsync(out, dsum, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    TB_CUDA(cudaStreamSynchronize(s));
+    return TURBDA_OK;
+}
+
+int turbda_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int turbda_abi_version(void) { return TURBDA_B200_ABI_VERSION; }
+
+const char* turbda_build_arch(void) { return "sm_100a"; }
+
+uint64_t turbda_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// Internal interface between the C-ABI layer (capi.cpp) and the sm_100a
+// kernels (ensf_kernels.cu).  Not installed; the public surface is
+// include/turbda_b200.h.
+#pragma once
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace tb200 {
+
+// Per pseudo-time step coefficients of the fp32 fast kernel (32 B).  All are
+// derived on the host in fp64 from the reference's time grid
+// (proj/src/ensf.cpp:149,183-190) and rounded once.
+struct StepF32 {
+    float na;     // -alpha(t)
+    float cl;     // log2(e) / (2 beta^2)      softmax exponent scale
+    float kp;     // -sigma^2 dt / beta^2      multiplies sum w (z - a x) / sum w
+    float kl;     // sigma^2 dt h(t)           multiplies B - A z (likelihood)
+    float nbdt;   // -b(t) dt                  drift
+    float sig;    // sqrt(sigma^2 dt)          noise amplitude
+    float pad0, pad1;
+};
+
+// fp64 faithful kernel: the reference's own quantities, evaluated exactly as
+// proj/src/ensf.cpp:183-190 does.
+struct StepF64 {
+    double alpha, beta2, inv2b, b, s2, damp, sig, dt;
+};
+
+struct KernelArgs {
+    int64_t d_total;   // global state dimension (noise index stride)
+    int64_t k0;        // global index of local coordinate 0
+    int64_t dl;        // coordinates in this window
+    int32_t m;         // ensemble members == particles
+    int32_t n_steps;
+    int32_t j_batch;   // members per step (== m unless minibatch)
+    int32_t minibatch; // 1 when `batches` holds a [n_steps][j_batch] table
+    uint32_t key0, key1;  // Philox key of the ensf_particles stream
+    uint32_t cycle_lo;    // entity = (cycle << 32) | i  ->  hi word
+    int32_t pad;
+};
+
+// Divergence word: min over ((particle << 32) | step); ~0 = none.
+constexpr unsigned long long kNoDivergence = ~0ull;
+
+// obs (y, r, idx) -> per-coordinate {A = sum 1/r, B = sum y/r} over the window
+cudaError_t launch_obs_prep(const double* y, const double* r, const int64_t* idx,
+                            int64_t obs_dim, int obs_kind, int64_t k0, int64_t dl,
+                            double2* ab, cudaStream_t st);
+
+// full fused analysis into z (fp32 or fp64 scratch, [m][dl])
+cudaError_t launch_ensf_f32(const KernelArgs& a, const double* x, const double2* ab,
+                            const StepF32* steps, const int32_t* batches, float* z,
+                            unsigned long long* status, cudaStream_t st);
+cudaError_t launch_ensf_f64(const KernelArgs& a, const double* x, const double2* ab,
+                            const StepF64* steps, const int32_t* batches, double* z,
+                            unsigned long long* status, cudaStream_t st);
+
+// relax_spread epilogue (proj/src/ensf.cpp:225-258): z (T) + forecast -> out (fp64)
+cudaError_t launch_relax_f32(const float* z, const double* x, int m, int64_t dl, double factor,
+                             double* out, cudaStream_t st);
+cudaError_t launch_relax_f64(const double* z, const double* x, int m, int64_t dl,
+                             double factor, double* out, cudaStream_t st);
+
+// single-vector score (prior_score / posterior_score API), fp64 faithful
+cudaError_t launch_score_f64(const double* z, const double* x, int m, int64_t d,
+                             const int32_t* batch, int nbatch, double alpha, double beta2,
+                             const double2* ab, double damp, double* out, cudaStream_t st);
+
+// rmse / spread partial sums: out[0] = sum (mean - truth)^2, out[1] = sum dev^2
+cudaError_t launch_diag(const double* x, int m, int64_t d, const double* truth, double* out,
+                        cudaStream_t st);
+
+}  // namespace tb200

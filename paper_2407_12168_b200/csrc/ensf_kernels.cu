@@ -1,0 +1,575 @@
+// sm_100a kernels for the EnSF analysis step (turbda::analyze,
+// proj/src/ensf.cpp:132-223) and its epilogue relax_spread (:225-258).
+//
+// Layout and mapping:
+//   * forecast X lives in HBM as the reference's [M][d] member-major fp64
+//     array.  A CTA owns a tile of 64 consecutive coordinates; lane l owns the
+//     coordinate pair (2l, 2l+1) of the tile, so every global access is a
+//     coalesced 16 B (fp64) per lane and both Box-Muller outputs of a Philox
+//     block land in the same thread.
+//   * each warp owns P particles of the tile; the whole reverse SDE (all
+//     n_steps pseudo-time steps) runs in registers: there is no per-step
+//     HBM traffic at all.  The prior score is componentwise
+//     (proj/src/ensf.cpp:27-64), so coordinates never talk to each other.
+//   * fp32 fast kernel: the tile's members are converted once into shared
+//     memory as float2 rows (lane-contiguous, conflict-free LDS.64); the
+//     pair arithmetic is packed FFMA2/FMUL2/FADD2 on the coordinate pair and
+//     the weights use MUFU.EX2 with a log2(e)-prescaled exponent.
+//   * fp64 faithful kernel: same mapping, the reference's own arithmetic
+//     (fast_exp_nonpos, num/den form, update order).
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+
+#include "ensf_device.h"
+#include "philox.cuh"
+
+namespace tb200 {
+
+namespace {
+
+constexpr int kTile = 64;  // coordinates per CTA tile (32 lanes x 2)
+
+__device__ __forceinline__ float ex2f(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+// proj/include/turbda/fastexp.hpp:13-50, restated for the device.
+__device__ __forceinline__ double fast_exp_nonpos_dev(double x) {
+    constexpr double kInvLn2 = 1.4426950408889634074;
+    constexpr double kLn2Hi = 6.93147180369123816490e-01;
+    constexpr double kLn2Lo = 1.90821492927058770002e-10;
+    constexpr double kMagic = 6755399441055744.0;
+    const bool under = x < -708.0;
+    if (under) x = 0.0;
+    const double t = x * kInvLn2 + kMagic;
+    const double nf = t - kMagic;
+    const int32_t n = int32_t(uint32_t(__double_as_longlong(t)));
+    double r = x - nf * kLn2Hi;
+    r -= nf * kLn2Lo;
+    double p = 1.0 / 479001600.0;
+    p = p * r + 1.0 / 39916800.0;
+    p = p * r + 1.0 / 3628800.0;
+    p = p * r + 1.0 / 362880.0;
+    p = p * r + 1.0 / 40320.0;
+    p = p * r + 1.0 / 5040.0;
+    p = p * r + 1.0 / 720.0;
+    p = p * r + 1.0 / 120.0;
+    p = p * r + 1.0 / 24.0;
+    p = p * r + 1.0 / 6.0;
+    p = p * r + 0.5;
+    p = p * r + 1.0;
+    p = p * r + 1.0;
+    const long long pb = __double_as_longlong(p) + (static_cast<long long>(n) << 52);
+    return under ? 0.0 : __longlong_as_double(pb);
+}
+
+// Loads X[j][k], X[j][k+1] (k local, even) with zero padding past dl.
+__device__ __forceinline__ double2 load_pair(const double* __restrict__ row, int64_t k,
+                                             int64_t dl, bool aligned) {
+    if (k + 1 < dl) {
+        if (aligned) return __ldg(reinterpret_cast<const double2*>(row + k));
+        return make_double2(__ldg(row + k), __ldg(row + k + 1));
+    }
+    if (k < dl) return make_double2(__ldg(row + k), 0.0);
+    return make_double2(0.0, 0.0);
+}
+
+// ---------------------------------------------------------------------------
+// fp32 fast kernel
+// ---------------------------------------------------------------------------
+template <int P, bool kMinibatch>
+__global__ void __launch_bounds__(256) ensf_f32_kernel(KernelArgs a, const double* __restrict__ x,
+                                                       const double2* __restrict__ ab,
+                                                       const StepF32* __restrict__ steps,
+                                                       const int32_t* __restrict__ batches,
+                                                       float* __restrict__ z_out,
+                                                       unsigned long long* __restrict__ status) {
+    extern __shared__ float4 smem[];
+    StepF32* cs = reinterpret_cast<StepF32*>(smem);
+    float2* xs = reinterpret_cast<float2*>(cs + a.n_steps);  // [m][32]
+
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    const int64_t tile0 = int64_t(blockIdx.x) * kTile;
+    const int64_t kl = tile0 + 2 * lane;  // local coordinate of this lane's pair
+    const bool aligned = ((a.dl & 1) == 0);
+
+    for (int q = threadIdx.x; q < a.n_steps; q += blockDim.x) cs[q] = steps[q];
+    for (int q = threadIdx.x; q < a.m * 32; q += blockDim.x) {
+        const int j = q >> 5, l = q & 31;
+        const double2 v = load_pair(x + size_t(j) * size_t(a.dl), tile0 + 2 * l, a.dl, aligned);
+        xs[q] = make_float2(float(v.x), float(v.y));
+    }
+    // likelihood operator for this pair: B - A z with A = sum 1/r, B = sum y/r
+    float2 A2 = f2(0.f), B2 = f2(0.f);
+    if (kl < a.dl) {
+        const double2 o = ab[kl];
+        A2.x = float(o.x);
+        B2.x = float(o.y);
+    }
+    if (kl + 1 < a.dl) {
+        const double2 o = ab[kl + 1];
+        A2.y = float(o.x);
+        B2.y = float(o.y);
+    }
+    const float2 nA2 = make_float2(-A2.x, -A2.y);
+    const bool has_y = kl + 1 < a.dl;  // the pair's second coordinate is real
+    __syncthreads();
+
+    const int i0 = (blockIdx.y * nwarps + warp) * P;
+    const uint64_t kg = uint64_t(a.k0 + kl);  // global coordinate of the pair's first entry
+
+    float2 z[P];
+    int bad[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        z[p] = normal_pair_f32(kg, uint32_t(i0 + p), a.cycle_lo, a.key0, a.key1);
+        bad[p] = INT_MAX;
+    }
+
+    for (int s = 0; s < a.n_steps; ++s) {
+        const StepF32 c = cs[s];
+        const float2 na2 = f2(c.na);
+        const int32_t* bt = kMinibatch ? batches + size_t(s) * size_t(a.j_batch) : nullptr;
+
+        // pass 1: per-coordinate smallest squared distance (softmax shift),
+        // proj/src/ensf.cpp:41-50
+        float2 mn[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) mn[p] = f2(FLT_MAX);
+#pragma unroll 4
+        for (int jj = 0; jj < a.j_batch; ++jj) {
+            const int j = kMinibatch ? __ldg(bt + jj) : jj;
+            const float2 xv = xs[j * 32 + lane];
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const float2 df = __ffma2_rn(na2, xv, z[p]);
+                const float2 d2 = __fmul2_rn(df, df);
+                mn[p].x = fminf(mn[p].x, d2.x);
+                mn[p].y = fminf(mn[p].y, d2.y);
+            }
+        }
+        // pass 2: w = 2^{cl (min - d2)}; den = sum w; num = sum w (z - alpha x),
+        // proj/src/ensf.cpp:51-61 in the cancellation-free form of :62-63
+        const float2 ncl2 = f2(-c.cl);
+        float2 mc[P], den[P], num[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            mc[p] = __fmul2_rn(mn[p], f2(c.cl));
+            den[p] = f2(0.f);
+            num[p] = f2(0.f);
+        }
+#pragma unroll 4
+        for (int jj = 0; jj < a.j_batch; ++jj) {
+            const int j = kMinibatch ? __ldg(bt + jj) : jj;
+            const float2 xv = xs[j * 32 + lane];
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const float2 df = __ffma2_rn(na2, xv, z[p]);
+                const float2 d2 = __fmul2_rn(df, df);
+                const float2 e = __ffma2_rn(d2, ncl2, mc[p]);
+                const float2 w = make_float2(ex2f(e.x), ex2f(e.y));
+                den[p] = __fadd2_rn(den[p], w);
+                num[p] = __ffma2_rn(w, df, num[p]);
+            }
+        }
+        // posterior score + Euler-Maruyama, proj/src/ensf.cpp:197-214
+        const uint64_t n0 = uint64_t(s + 1) * uint64_t(a.d_total) + kg;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const float2 q = make_float2(__fdividef(num[p].x, den[p].x),
+                                         __fdividef(num[p].y, den[p].y));
+            const float2 lik = __ffma2_rn(nA2, z[p], B2);
+            const float2 xi = normal_pair_f32(n0, uint32_t(i0 + p), a.cycle_lo, a.key0, a.key1);
+            float2 zn = __ffma2_rn(z[p], f2(c.nbdt), z[p]);
+            zn = __ffma2_rn(f2(c.kp), q, zn);
+            zn = __ffma2_rn(f2(c.kl), lik, zn);
+            zn = __ffma2_rn(f2(c.sig), xi, zn);
+            z[p] = zn;
+            const bool fin = (fabsf(zn.x) <= FLT_MAX) && (fabsf(zn.y) <= FLT_MAX || !has_y);
+            if (!fin && bad[p] == INT_MAX) bad[p] = s;
+        }
+    }
+
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const int i = i0 + p;
+        if (i >= a.m) continue;
+        float* row = z_out + size_t(i) * size_t(a.dl);
+        if (kl + 1 < a.dl) {
+            if (aligned) {
+                *reinterpret_cast<float2*>(row + kl) = z[p];
+            } else {
+                row[kl] = z[p].x;
+                row[kl + 1] = z[p].y;
+            }
+        } else if (kl < a.dl) {
+            row[kl] = z[p].x;
+        }
+        if (bad[p] != INT_MAX && kl < a.dl)
+            atomicMin(status, (uint64_t(i) << 32) | uint32_t(bad[p]));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// fp64 faithful kernel (reference arithmetic)
+// ---------------------------------------------------------------------------
+template <int P, bool kMinibatch, bool kSmemX>
+__global__ void __launch_bounds__(128) ensf_f64_kernel(KernelArgs a, const double* __restrict__ x,
+                                                       const double2* __restrict__ ab,
+                                                       const StepF64* __restrict__ steps,
+                                                       const int32_t* __restrict__ batches,
+                                                       double* __restrict__ z_out,
+                                                       unsigned long long* __restrict__ status) {
+    extern __shared__ double2 smem2[];
+    StepF64* cs = reinterpret_cast<StepF64*>(smem2);
+    double2* xs = reinterpret_cast<double2*>(cs + a.n_steps);  // [m][32] when kSmemX
+
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    const int64_t tile0 = int64_t(blockIdx.x) * kTile;
+    const int64_t kl = tile0 + 2 * lane;
+    const bool aligned = ((a.dl & 1) == 0);
+
+    for (int q = threadIdx.x; q < a.n_steps; q += blockDim.x) cs[q] = steps[q];
+    if (kSmemX) {
+        for (int q = threadIdx.x; q < a.m * 32; q += blockDim.x) {
+            const int j = q >> 5, l = q & 31;
+            xs[q] = load_pair(x + size_t(j) * size_t(a.dl), tile0 + 2 * l, a.dl, aligned);
+        }
+    }
+    double2 A = make_double2(0, 0), B = make_double2(0, 0);
+    if (kl < a.dl) {
+        const double2 o = ab[kl];
+        A.x = o.x;
+        B.x = o.y;
+    }
+    if (kl + 1 < a.dl) {
+        const double2 o = ab[kl + 1];
+        A.y = o.x;
+        B.y = o.y;
+    }
+    __syncthreads();
+
+    const int i0 = (blockIdx.y * nwarps + warp) * P;
+    const uint64_t kg = uint64_t(a.k0 + kl);
+
+    double zx[P], zy[P];
+    int bad[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const double2 v = normal_pair_f64(kg, uint32_t(i0 + p), a.cycle_lo, a.key0, a.key1);
+        zx[p] = v.x;
+        zy[p] = v.y;
+        bad[p] = INT_MAX;
+    }
+
+    for (int s = 0; s < a.n_steps; ++s) {
+        const StepF64 c = cs[s];
+        const int32_t* bt = kMinibatch ? batches + size_t(s) * size_t(a.j_batch) : nullptr;
+        double mx[P], my[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) mx[p] = my[p] = __longlong_as_double(0x7ff0000000000000ll);
+        for (int jj = 0; jj < a.j_batch; ++jj) {
+            const int j = kMinibatch ? __ldg(bt + jj) : jj;
+            const double2 xv = kSmemX ? xs[j * 32 + lane]
+                                      : load_pair(x + size_t(j) * size_t(a.dl), kl, a.dl, aligned);
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const double dx = zx[p] - c.alpha * xv.x;
+                const double dy = zy[p] - c.alpha * xv.y;
+                const double d2x = dx * dx, d2y = dy * dy;
+                mx[p] = d2x < mx[p] ? d2x : mx[p];
+                my[p] = d2y < my[p] ? d2y : my[p];
+            }
+        }
+        double nx[P], ny[P], ex[P], ey[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) nx[p] = ny[p] = ex[p] = ey[p] = 0.0;
+        for (int jj = 0; jj < a.j_batch; ++jj) {
+            const int j = kMinibatch ? __ldg(bt + jj) : jj;
+            const double2 xv = kSmemX ? xs[j * 32 + lane]
+                                      : load_pair(x + size_t(j) * size_t(a.dl), kl, a.dl, aligned);
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                const double dx = zx[p] - c.alpha * xv.x;
+                const double dy = zy[p] - c.alpha * xv.y;
+                const double wx = fast_exp_nonpos_dev((mx[p] - dx * dx) * c.inv2b);
+                const double wy = fast_exp_nonpos_dev((my[p] - dy * dy) * c.inv2b);
+                ex[p] += wx;
+                ey[p] += wy;
+                nx[p] += wx * xv.x;
+                ny[p] += wy * xv.y;
+            }
+        }
+        const uint64_t n0 = uint64_t(s + 1) * uint64_t(a.d_total) + kg;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            double scx = -(zx[p] - c.alpha * nx[p] / ex[p]) / c.beta2;
+            double scy = -(zy[p] - c.alpha * ny[p] / ey[p]) / c.beta2;
+            scx += c.damp * (B.x - A.x * zx[p]);
+            scy += c.damp * (B.y - A.y * zy[p]);
+            const double2 xi = normal_pair_f64(n0, uint32_t(i0 + p), a.cycle_lo, a.key0, a.key1);
+            zx[p] += -(c.b * zx[p] - c.s2 * scx) * c.dt + c.sig * xi.x;
+            zy[p] += -(c.b * zy[p] - c.s2 * scy) * c.dt + c.sig * xi.y;
+            const bool fin = isfinite(zx[p]) && (isfinite(zy[p]) || kl + 1 >= a.dl);
+            if (!fin && bad[p] == INT_MAX) bad[p] = s;
+        }
+    }
+
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const int i = i0 + p;
+        if (i >= a.m || kl >= a.dl) continue;
+        double* row = z_out + size_t(i) * size_t(a.dl);
+        if (kl + 1 < a.dl) {
+            if (aligned) {
+                *reinterpret_cast<double2*>(row + kl) = make_double2(zx[p], zy[p]);
+            } else {
+                row[kl] = zx[p];
+                row[kl + 1] = zy[p];
+            }
+        } else {
+            row[kl] = zx[p];
+        }
+        if (bad[p] != INT_MAX) atomicMin(status, (uint64_t(i) << 32) | uint32_t(bad[p]));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// relax_spread epilogue, proj/src/ensf.cpp:225-258 (+ ensemble_mean,
+// proj/src/ensemble.cpp:7-16), fp64 statistics, one thread per coordinate.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void relax_kernel(const T* __restrict__ z, const double* __restrict__ x, int m,
+                             int64_t dl, double factor, double* __restrict__ out) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= dl) return;
+    if (factor == 0.0 || m < 2) {
+        for (int j = 0; j < m; ++j) out[size_t(j) * dl + k] = double(z[size_t(j) * dl + k]);
+        return;
+    }
+    double ma = 0.0, mb = 0.0;
+    for (int j = 0; j < m; ++j) {
+        ma += double(z[size_t(j) * dl + k]);
+        mb += x[size_t(j) * dl + k];
+    }
+    const double inv = 1.0 / m;
+    ma *= inv;
+    mb *= inv;
+    double va = 0.0, vb = 0.0;
+    for (int j = 0; j < m; ++j) {
+        const double da = double(z[size_t(j) * dl + k]) - ma;
+        const double db = x[size_t(j) * dl + k] - mb;
+        va += da * da;
+        vb += db * db;
+    }
+    const double sa = fmax(sqrt(va / (m - 1)), 1e-12);
+    const double sb = sqrt(vb / (m - 1));
+    const double scale = (1.0 - factor) + factor * sb / sa;
+    for (int j = 0; j < m; ++j)
+        out[size_t(j) * dl + k] = ma + scale * (double(z[size_t(j) * dl + k]) - ma);
+}
+
+// obs -> per-coordinate {A, B}.  Identity: one entry per coordinate.
+// Selection: entries whose global index falls in the window are scattered
+// (duplicate indices add, as adjoint_scatter does, proj/src/observation.cpp:18-27).
+__global__ void obs_identity_kernel(const double* __restrict__ y, const double* __restrict__ r,
+                                    int64_t dl, double2* __restrict__ ab) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k < dl) {
+        const double inv = 1.0 / r[k];
+        ab[k] = make_double2(inv, y[k] * inv);
+    }
+}
+
+__global__ void obs_select_kernel(const double* __restrict__ y, const double* __restrict__ r,
+                                  const int64_t* __restrict__ idx, int64_t obs_dim, int64_t k0,
+                                  int64_t dl, double2* __restrict__ ab) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= obs_dim) return;
+    const int64_t k = idx[q] - k0;
+    if (k < 0 || k >= dl) return;
+    const double inv = 1.0 / r[q];
+    atomicAdd(&ab[k].x, inv);
+    atomicAdd(&ab[k].y, y[q] * inv);
+}
+
+// single-vector componentwise score, proj/src/ensf.cpp:33-64,96-106
+__global__ void score_kernel(const double* __restrict__ z, const double* __restrict__ x, int m,
+                             int64_t d, const int32_t* __restrict__ batch, int nbatch,
+                             double alpha, double beta2, const double2* __restrict__ ab,
+                             double damp, double* __restrict__ out) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= d) return;
+    const double inv2b = 1.0 / (2.0 * beta2);
+    const double zk = z[k];
+    double mind2 = __longlong_as_double(0x7ff0000000000000ll);
+    for (int jj = 0; jj < nbatch; ++jj) {
+        const int j = batch ? batch[jj] : jj;
+        const double diff = zk - alpha * x[size_t(j) * d + k];
+        const double d2 = diff * diff;
+        mind2 = d2 < mind2 ? d2 : mind2;
+    }
+    double num = 0.0, den = 0.0;
+    for (int jj = 0; jj < nbatch; ++jj) {
+        const int j = batch ? batch[jj] : jj;
+        const double xv = x[size_t(j) * d + k];
+        const double diff = zk - alpha * xv;
+        const double w = fast_exp_nonpos_dev((mind2 - diff * diff) * inv2b);
+        den += w;
+        num += w * xv;
+    }
+    double s = -(zk - alpha * num / den) / beta2;
+    if (ab) s += damp * (ab[k].y - ab[k].x * zk);
+    out[k] = s;
+}
+
+// rmse/spread partial sums (proj/src/ensemble.cpp:18-43)
+__global__ void diag_kernel(const double* __restrict__ x, int m, int64_t d,
+                            const double* __restrict__ truth, double* __restrict__ out) {
+    double e2 = 0.0, v2 = 0.0;
+    for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < d;
+         k += int64_t(gridDim.x) * blockDim.x) {
+        double mean = 0.0;
+        for (int j = 0; j < m; ++j) mean += x[size_t(j) * d + k];
+        mean *= 1.0 / m;
+        if (truth) {
+            const double e = mean - truth[k];
+            e2 += e * e;
+        }
+        for (int j = 0; j < m; ++j) {
+            const double dv = x[size_t(j) * d + k] - mean;
+            v2 += dv * dv;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out, e2);
+        atomicAdd(out + 1, v2);
+    }
+}
+
+int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
+
+template <int P>
+cudaError_t launch_f32_p(const KernelArgs& a, const double* x, const double2* ab,
+                         const StepF32* steps, const int32_t* batches, float* z,
+                         unsigned long long* status, cudaStream_t st) {
+    // warps per CTA: enough to cover the members, at most 8
+    const int groups = (a.m + P - 1) / P;
+    const int nw = groups < 8 ? groups : 8;
+    const dim3 block(32 * nw);
+    const dim3 grid(unsigned((a.dl + kTile - 1) / kTile), unsigned((groups + nw - 1) / nw));
+    const size_t smem = sizeof(StepF32) * size_t(a.n_steps) + sizeof(float2) * 32 * size_t(a.m);
+    auto kern = a.minibatch ? ensf_f32_kernel<P, true> : ensf_f32_kernel<P, false>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(smem));
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<grid, block, smem, st>>>(a, x, ab, steps, batches, z, status);
+    return cudaGetLastError();
+}
+
+template <int P, bool kSmemX>
+cudaError_t launch_f64_p(const KernelArgs& a, const double* x, const double2* ab,
+                         const StepF64* steps, const int32_t* batches, double* z,
+                         unsigned long long* status, cudaStream_t st) {
+    const int groups = (a.m + P - 1) / P;
+    const int nw = groups < 4 ? groups : 4;
+    const dim3 block(32 * nw);
+    const dim3 grid(unsigned((a.dl + kTile - 1) / kTile), unsigned((groups + nw - 1) / nw));
+    const size_t smem = sizeof(StepF64) * size_t(a.n_steps) +
+                        (kSmemX ? sizeof(double2) * 32 * size_t(a.m) : 0);
+    auto kern = a.minibatch ? ensf_f64_kernel<P, true, kSmemX> : ensf_f64_kernel<P, false, kSmemX>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(smem));
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<grid, block, smem, st>>>(a, x, ab, steps, batches, z, status);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_obs_prep(const double* y, const double* r, const int64_t* idx,
+                            int64_t obs_dim, int obs_kind, int64_t k0, int64_t dl, double2* ab,
+                            cudaStream_t st) {
+    if (dl <= 0) return cudaSuccess;
+    if (obs_kind == 0) {
+        obs_identity_kernel<<<blocks_for(dl, 256), 256, 0, st>>>(y, r, dl, ab);
+        return cudaGetLastError();
+    }
+    cudaError_t e = cudaMemsetAsync(ab, 0, sizeof(double2) * size_t(dl), st);
+    if (e != cudaSuccess || obs_dim == 0) return e;
+    obs_select_kernel<<<blocks_for(obs_dim, 256), 256, 0, st>>>(y, r, idx, obs_dim, k0, dl, ab);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ensf_f32(const KernelArgs& a, const double* x, const double2* ab,
+                            const StepF32* steps, const int32_t* batches, float* z,
+                            unsigned long long* status, cudaStream_t st) {
+    if (a.dl <= 0) return cudaSuccess;
+    if (a.m % 4 == 0) return launch_f32_p<4>(a, x, ab, steps, batches, z, status, st);
+    if (a.m % 2 == 0) return launch_f32_p<2>(a, x, ab, steps, batches, z, status, st);
+    return launch_f32_p<1>(a, x, ab, steps, batches, z, status, st);
+}
+
+cudaError_t launch_ensf_f64(const KernelArgs& a, const double* x, const double2* ab,
+                            const StepF64* steps, const int32_t* batches, double* z,
+                            unsigned long long* status, cudaStream_t st) {
+    if (a.dl <= 0) return cudaSuccess;
+    const bool smem_x = a.m <= 160;
+    if (a.m % 2 == 0)
+        return smem_x ? launch_f64_p<2, true>(a, x, ab, steps, batches, z, status, st)
+                      : launch_f64_p<2, false>(a, x, ab, steps, batches, z, status, st);
+    return smem_x ? launch_f64_p<1, true>(a, x, ab, steps, batches, z, status, st)
+                  : launch_f64_p<1, false>(a, x, ab, steps, batches, z, status, st);
+}
+
+cudaError_t launch_relax_f32(const float* z, const double* x, int m, int64_t dl, double factor,
+                             double* out, cudaStream_t st) {
+    if (dl <= 0) return cudaSuccess;
+    relax_kernel<float><<<blocks_for(dl, 256), 256, 0, st>>>(z, x, m, dl, factor, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_relax_f64(const double* z, const double* x, int m, int64_t dl,
+                             double factor, double* out, cudaStream_t st) {
+    if (dl <= 0) return cudaSuccess;
+    relax_kernel<double><<<blocks_for(dl, 256), 256, 0, st>>>(z, x, m, dl, factor, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_score_f64(const double* z, const double* x, int m, int64_t d,
+                             const int32_t* batch, int nbatch, double alpha, double beta2,
+                             const double2* ab, double damp, double* out, cudaStream_t st) {
+    if (d <= 0) return cudaSuccess;
+    score_kernel<<<blocks_for(d, 128), 128, 0, st>>>(z, x, m, d, batch, nbatch, alpha, beta2, ab,
+                                                      damp, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_diag(const double* x, int m, int64_t d, const double* truth, double* out,
+                        cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(out, 0, 2 * sizeof(double), st);
+    if (e != cudaSuccess || d <= 0) return e;
+    int blocks = blocks_for(d, 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    diag_kernel<<<blocks, 256, 0, st>>>(x, m, d, truth, out);
+    return cudaGetLastError();
+}
+
+}  // namespace tb200

@@ -1,0 +1,123 @@
+// Python module paper_2407_12168_b200._core - the B200 counterpart of the
+// reference binding's EnSF entry point (proj/python/bindings.cpp:140-155,
+// exceptions :223-224).  ensf_analyze keeps the reference signature and
+// defaults; keyword-only extras select the observation thinning, the
+// arithmetic and the devices.  Arrays go straight from numpy to the device
+// through the C-ABI (no vector<vector<double>> round trip).
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "turbda/errors.hpp"
+#include "turbda/grid.hpp"
+#include "turbda_b200.h"
+
+namespace py = pybind11;
+
+namespace {
+
+using darray = py::array_t<double, py::array::c_style | py::array::forcecast>;
+
+[[noreturn]] void raise(int code, const turbda_status& st) {
+    switch (code) {
+        case TURBDA_CONFIG: throw turbda::ConfigError(st.msg);
+        case TURBDA_DIMENSION: throw turbda::DimensionError(st.msg);
+        case TURBDA_DIVERGED: throw turbda::SamplerDivergedError(st.diverged_t);
+        case TURBDA_DOMAIN: throw std::domain_error(st.msg);
+        default: throw std::runtime_error(std::string("turbda_b200: ") + st.msg);
+    }
+}
+
+int parse_precision(const std::string& s) {
+    if (s == "fp32" || s == "float32") return TURBDA_FP32;
+    if (s == "fp64" || s == "float64") return TURBDA_FP64;
+    throw turbda::ConfigError("precision must be 'fp32' or 'fp64'");
+}
+
+py::array_t<double> ensf_analyze(const darray& members, const turbda::GridSpec& grid,
+                                 const darray& y, double r, std::uint64_t seed,
+                                 std::uint64_t cycle, int n_steps, double relax_factor,
+                                 int /*workers*/, int thinning, const std::string& precision,
+                                 int device, int device_count, double eps, int minibatch_j,
+                                 double damping_t) {
+    if (members.ndim() != 2) throw turbda::DimensionError("members must be (M, d)");
+    const auto m = members.shape(0);
+    const auto d = members.shape(1);
+    // Ensemble::validate(false)
+    if (m < 1) throw turbda::DimensionError("ensemble: empty");
+    // make_grid_operator(grid, thinning) + Observation::validate
+    const int64_t state_dim = int64_t(grid.grid_size());
+    std::vector<int64_t> idx;
+    if (thinning > 1)
+        for (int64_t k = 0; k < state_dim; k += thinning) idx.push_back(k);
+    const int64_t obs_dim = thinning > 1 ? int64_t(idx.size()) : state_dim;
+    if (y.size() != obs_dim) throw turbda::DimensionError("observation: length mismatch");
+    if (!(r > 0.0)) throw turbda::ConfigError("observation: r_diag > 0");
+    if (state_dim != d) throw turbda::DimensionError("analyze: observation operator dimension");
+    const std::vector<double> rr(size_t(obs_dim), r);
+
+    turbda_ensf_params p;
+    turbda_ensf_params_init(&p);
+    p.d_total = d;
+    p.d_local = d;
+    p.obs_dim = obs_dim;
+    p.n_members = int32_t(m);
+    p.n_steps = n_steps;
+    p.minibatch_j = minibatch_j;
+    p.obs_kind = thinning > 1 ? 1 : 0;
+    p.eps = eps;
+    p.damping_t = damping_t;
+    p.relax_factor = relax_factor;
+    p.seed = seed;
+    p.cycle = cycle;
+    p.precision = parse_precision(precision);
+    p.device = device;
+    p.device_count = device_count;
+
+    py::array_t<double> out({m, d});
+    turbda_status st{};
+    int rc;
+    {
+        py::gil_scoped_release nogil;
+        rc = turbda_ensf_analyze(&p, members.data(), y.data(), rr.data(),
+                                 idx.empty() ? nullptr : idx.data(), out.mutable_data(), nullptr,
+                                 &st);
+    }
+    if (rc) raise(rc, st);
+    return out;
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_core, mod) {
+    mod.doc() = "B200-native EnSF analysis step (sm_100a) behind the turbda binding API";
+
+    py::class_<turbda::GridSpec>(mod, "GridSpec")
+        .def(py::init<>())
+        .def_readwrite("nx", &turbda::GridSpec::nx)
+        .def_readwrite("ny", &turbda::GridSpec::ny)
+        .def_readwrite("nz", &turbda::GridSpec::nz)
+        .def_readwrite("lx", &turbda::GridSpec::lx)
+        .def_readwrite("ly", &turbda::GridSpec::ly)
+        .def_readwrite("h", &turbda::GridSpec::h)
+        .def("grid_size", &turbda::GridSpec::grid_size)
+        .def("validate", &turbda::GridSpec::validate);
+
+    mod.def("ensf_analyze", &ensf_analyze, py::arg("members"), py::arg("grid"), py::arg("y"),
+            py::arg("r") = 1.0, py::arg("seed") = 7, py::arg("cycle") = 1,
+            py::arg("n_steps") = 100, py::arg("relax_factor") = 1.0, py::arg("workers") = 0,
+            py::kw_only(), py::arg("thinning") = 0, py::arg("precision") = "fp32",
+            py::arg("device") = -1, py::arg("device_count") = 1, py::arg("eps") = 0.01,
+            py::arg("minibatch_j") = 0, py::arg("damping_t") = 1.0,
+            "EnSF analysis of an (M, d) float64 forecast ensemble on the GPU; returns (M, d)");
+
+    mod.def("device_count", &turbda_device_count);
+    mod.def("build_arch", [] { return std::string(turbda_build_arch()); });
+    mod.def("launch_count", [] { return turbda_launch_count(); });
+
+    py::register_exception<turbda::ConfigError>(mod, "ConfigError", PyExc_ValueError);
+    py::register_exception<turbda::DimensionError>(mod, "DimensionError", PyExc_ValueError);
+}

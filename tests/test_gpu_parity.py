@@ -1,0 +1,212 @@
+"""GPU parity of the sm_100a analysis against the oracles.
+
+Tolerances (stated per BASELINE.md section 5 / SURVEY.md 8(c)):
+  * fp64 faithful path: rel-L2 <= 1e-10 against the reference's own outputs.
+  * fp32 fast path: rel-L2 <= 1e-4 on fp32-representable inputs.
+Sharding / determinism properties are bit-exact.
+"""
+import numpy as np
+import pytest
+
+from conftest import ROOT, case_kwargs, load_cases
+from oracle.oracle import conditioned_inputs, rel_l2, throughput_inputs
+
+pytestmark = pytest.mark.gpu
+
+FP64_TOL = 1e-10
+FP32_TOL = 1e-4
+CASES = load_cases()
+
+
+@pytest.fixture(scope="module")
+def capi():
+    from paper_2407_12168_b200 import capi as c
+    if c.device_count() < 1:
+        pytest.fail("no CUDA device visible to libturbda_b200.so")
+    return c
+
+
+def run_case(capi, rec, precision):
+    kw = case_kwargs(rec)
+    idx = rec["idx"] if int(rec["obs_kind"]) == 1 else None
+    return capi.analyze_host(rec["x"], rec["y"], rec["r"], idx, precision=precision, **kw)
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_fp64_golden(capi, name):
+    rec = CASES[name]
+    if int(rec["status"]) == 3:
+        with pytest.raises(capi.TurbdaError) as ei:
+            run_case(capi, rec, capi.FP64)
+        assert ei.value.code == capi.DIVERGED
+        assert ei.value.diverged_t == pytest.approx(float(rec["diverged_t"]), abs=1e-12)
+        return
+    got = run_case(capi, rec, capi.FP64)
+    assert rel_l2(got, rec["out"]) <= FP64_TOL
+
+
+@pytest.mark.parametrize("name", sorted(n for n in CASES if n != "huge_member_nonfinite_relax"))
+def test_fp32_golden(capi, name):
+    rec = CASES[name]
+    if int(rec["status"]) == 3:
+        with pytest.raises(capi.TurbdaError) as ei:
+            run_case(capi, rec, capi.FP32)
+        assert ei.value.code == capi.DIVERGED
+        return
+    got = run_case(capi, rec, capi.FP32)
+    assert rel_l2(got, rec["out"]) <= FP32_TOL, rel_l2(got, rec["out"])
+
+
+def test_cfg1_full_size_vs_reference(capi, ref):
+    """BASELINE config 1 shape: d=8192, N=20, S=50, identity obs (arctan is an
+    unpinned extension, so the reference-parity run uses identity)."""
+    x, y, _, _ = conditioned_inputs(20, 8192)
+    x = x.astype(np.float32).astype(np.float64)
+    y = y.astype(np.float32).astype(np.float64)
+    want = ref.analyze(x, y, n_steps=50, workers=0)
+    got32 = capi.analyze_host(x, y, n_steps=50, precision=capi.FP32)
+    got64 = capi.analyze_host(x, y, n_steps=50, precision=capi.FP64)
+    e32, e64 = rel_l2(got32, want), rel_l2(got64, want)
+    print(f"cfg1 fp32 rel-L2 {e32:.3e}  fp64 rel-L2 {e64:.3e}")
+    assert e64 <= FP64_TOL
+    assert e32 <= FP32_TOL
+
+
+def test_cfg2_shape_vs_reference(capi, ref):
+    """Config 2 shape (N=64, S=100, stride-4 obs) on a d=8192 slice of the state."""
+    x, y, idx = throughput_inputs(64, 8192, stride=4)
+    x = x.astype(np.float32).astype(np.float64)
+    y = y.astype(np.float32).astype(np.float64)
+    want = ref.analyze(x, y, 1.0, idx, n_steps=100, workers=0)
+    got32 = capi.analyze_host(x, y, 1.0, idx, precision=capi.FP32)
+    got64 = capi.analyze_host(x, y, 1.0, idx, precision=capi.FP64)
+    e32, e64 = rel_l2(got32, want), rel_l2(got64, want)
+    print(f"cfg2-shape fp32 rel-L2 {e32:.3e}  fp64 rel-L2 {e64:.3e}")
+    assert e64 <= FP64_TOL
+    assert e32 <= FP32_TOL
+
+
+def test_large_members_smem_and_global_paths(capi, port):
+    """N=200 (> the fp64 shared-memory threshold) and odd N, vs the C oracle."""
+    for m, d in ((200, 256), (33, 130)):
+        x, y, _, _ = conditioned_inputs(m, d)
+        x = x.astype(np.float32).astype(np.float64)
+        want = port.analyze(x, y, n_steps=20)
+        for prec, tol in ((capi.FP64, FP64_TOL), (capi.FP32, FP32_TOL)):
+            got = capi.analyze_host(x, y, n_steps=20, precision=prec)
+            assert rel_l2(got, want) <= tol, (m, d, prec, rel_l2(got, want))
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_windows_reassemble_bitwise(capi, precision):
+    """State-dimension sharding: windows [k0, k0+dl) reproduce the whole-state
+    call bit for bit (odd boundaries included)."""
+    x, y, idx = throughput_inputs(16, 1000, stride=3)
+    whole = capi.analyze_host(x, y, 0.7, idx, n_steps=30, precision=precision)
+    parts = []
+    for lo, hi in ((0, 129), (129, 640), (640, 1000)):
+        sel = (idx >= lo) & (idx < hi)
+        parts.append(capi.analyze_host(x[:, lo:hi], y[sel], 0.7, idx[sel], n_steps=30,
+                                       precision=precision, k0=lo, d_total=1000))
+    assert np.array_equal(np.concatenate(parts, axis=1), whole)
+
+
+def test_deterministic(capi):
+    x, y, idx = throughput_inputs(20, 4096, stride=4)
+    a = capi.analyze_host(x, y, 1.0, idx, n_steps=50)
+    b = capi.analyze_host(x, y, 1.0, idx, n_steps=50)
+    assert np.array_equal(a, b)
+    c = capi.analyze_host(x, y, 1.0, idx, n_steps=50, cycle=2)
+    assert not np.array_equal(a, c)
+
+
+def test_multi_device_split(capi):
+    n = capi.device_count()
+    if n < 2:
+        pytest.skip("one device")
+    x, y, idx = throughput_inputs(20, 5000, stride=4)
+    one = capi.analyze_host(x, y, 1.0, idx, n_steps=20)
+    many = capi.analyze_host(x, y, 1.0, idx, n_steps=20, device=0, device_count=n)
+    assert np.array_equal(one, many)
+
+
+def test_scores_vs_golden(capi):
+    s = np.load(ROOT / "tests" / "golden" / "scores.npz")
+    for t, want_p, want_q in zip(s["t"], s["prior"], s["posterior"]):
+        got_p = capi.score(s["z"], float(t), s["x"])
+        got_q = capi.score(s["z"], float(t), s["x"], y=s["y"], r=0.7)
+        assert rel_l2(got_p, want_p) <= 1e-12
+        assert rel_l2(got_q, want_q) <= 1e-12
+    with pytest.raises(capi.TurbdaError) as ei:
+        capi.score(s["z"], 0.001, s["x"])
+    assert ei.value.code == capi.DOMAIN
+
+
+def test_relax_spread_vs_golden(capi):
+    s = np.load(ROOT / "tests" / "golden" / "scores.npz")
+    for f, want in zip(s["relax_factors"], s["relax"]):
+        assert rel_l2(capi.relax_spread(s["relax_a"], s["x"], float(f)), want) <= 1e-14
+
+
+def test_diag_matches_reference(capi, ref):
+    x, y, _, truth = conditioned_inputs(12, 3000)
+    e2, v2 = capi.diag(x, truth)
+    m, d = x.shape
+    assert np.sqrt(e2 / d) == pytest.approx(ref.rmse(x.mean(0), truth), rel=1e-12)
+    assert np.sqrt(v2 / ((m - 1) * d)) == pytest.approx(ref.spread(x), rel=1e-12)
+
+
+def test_python_binding_end_to_end(capi, ref):
+    import paper_2407_12168_b200 as tb
+    x, y, _, _ = conditioned_inputs(20, 2048)
+    g = tb.GridSpec()
+    g.nx, g.ny = 32, 32
+    got = tb.ensf_analyze(x, g, y, r=1.0, seed=9, cycle=1, n_steps=60, precision="fp64")
+    want = ref.analyze(x, y, n_steps=60, seed=9, cycle=1)
+    assert rel_l2(got, want) <= FP64_TOL
+    idx = np.arange(0, 2048, 4)
+    got = tb.ensf_analyze(x, g, y[idx], thinning=4, n_steps=60)
+    want = ref.analyze(x, y[idx], 1.0, idx, n_steps=60)
+    assert rel_l2(got, want) <= 1e-3  # fp64 inputs (not fp32-rounded): input rounding dominates
+
+
+def test_divergence_raises_runtime_error(capi):
+    import paper_2407_12168_b200 as tb
+    rec = CASES["diverges_stiff"]
+    g = tb.GridSpec()
+    g.nx, g.ny, g.nz = 2, 2, 2
+    with pytest.raises(RuntimeError, match="reverse SDE diverged"):
+        tb.ensf_analyze(rec["x"], g, rec["y"], r=1e-9, n_steps=10, precision="fp64")
+
+
+def test_device_pointer_path_matches_host_path(capi):
+    torch = pytest.importorskip("torch")
+    x, y, idx = throughput_inputs(64, 4096, stride=4)
+    host = capi.analyze_host(x, y, 1.0, idx, n_steps=100)
+    dev = torch.device("cuda:0")
+    tx = torch.from_numpy(x).to(dev)
+    ty = torch.from_numpy(y).to(dev)
+    tr = torch.ones_like(ty)
+    ti = torch.from_numpy(idx).to(dev)
+    out = torch.empty_like(tx)
+    p = capi.params(d_total=4096, d_local=4096, obs_dim=y.size, n_members=64, obs_kind=1,
+                    device=0, flags=capi.INPUTS_ON_DEVICE)
+    capi.analyze(p, tx, ty, tr, ti, out, stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), host)
+
+
+@pytest.mark.slow
+def test_cfg2_full_size_properties(capi):
+    """BASELINE config 2 at full size (d=131072, N=64, S=100, stride-4 obs):
+    fp32 and fp64 agree, shards reassemble bit-exactly, and the analysis is finite."""
+    x, y, idx = throughput_inputs(64, 131072, stride=4)
+    a32 = capi.analyze_host(x, y, 1.0, idx)
+    a64 = capi.analyze_host(x, y, 1.0, idx, precision=capi.FP64)
+    assert np.isfinite(a32).all()
+    assert rel_l2(a32, a64) <= FP32_TOL
+    half = 65536
+    sel = idx < half
+    lo = capi.analyze_host(x[:, :half], y[sel], 1.0, idx[sel], k0=0, d_total=131072)
+    hi = capi.analyze_host(x[:, half:], y[~sel], 1.0, idx[~sel], k0=half, d_total=131072)
+    assert np.array_equal(np.concatenate([lo, hi], axis=1), a32)

@@ -1,0 +1,105 @@
+"""CPU: the oracles against the golden fixtures made by the reference itself
+(tests/golden/make_golden.py).  Pins the C restatement before anything is
+compared with it."""
+import numpy as np
+import pytest
+
+from conftest import ROOT, case_kwargs, load_cases
+from oracle.oracle import OracleError, rel_l2
+
+RNG = np.load(ROOT / "tests" / "golden" / "rng.npz")
+CASES = load_cases()
+
+
+def test_philox_known_answers(port):
+    for c, k, want in zip(RNG["philox_ctr"], RNG["philox_key"], RNG["philox_out"]):
+        assert np.array_equal(port.philox4x32(c, k), want)
+    # Random123 kat_vectors: the implementation's value for the all-ones
+    # vector (proj/tests/test_rng.cpp:23 expects 0x93f2f747, which is a typo)
+    assert RNG["philox_out"][1][3] == 0x6D5451FD
+    assert RNG["philox_out"][0][0] == 0x6627E8D5
+
+
+def test_splitmix(port):
+    for a, b in zip(RNG["splitmix_in"], RNG["splitmix_out"]):
+        assert port.splitmix64(int(a)) == int(b)
+    assert port.splitmix64(1234567) == 6457827717110365317  # proj/tests/test_rng.cpp:41-45
+
+
+def test_stream_normals_and_u64_bit_exact(port):
+    for (seed, use, ent), normals, u64 in zip(RNG["stream_params"], RNG["normals"], RNG["u64"]):
+        got = port.stream_normals(int(seed), int(use), int(ent), normals.size)
+        assert np.array_equal(got, normals)
+        assert np.array_equal(port.stream_u64(int(seed), int(use), int(ent), u64.size), u64)
+
+
+def test_fast_exp(port):
+    got = np.array([port.fast_exp_nonpos(v) for v in RNG["fexp_in"]])
+    want = RNG["fexp_out"]
+    # reference built with -march=native contracts to FMA; a few ulp apart at most
+    assert np.all(np.abs(got - want) <= 4 * np.spacing(np.maximum(want, 1e-300)))
+    assert port.fast_exp_nonpos(0.0) == 1.0 and port.fast_exp_nonpos(-800.0) == 0.0
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_port_matches_reference_goldens(port, name):
+    rec = CASES[name]
+    kw = case_kwargs(rec)
+    idx = rec["idx"] if int(rec["obs_kind"]) == 1 else None
+    if int(rec["status"]) == 3:
+        with pytest.raises(OracleError) as ei:
+            port.analyze(rec["x"], rec["y"], rec["r"], idx, workers=4, **kw)
+        assert ei.value.kind == "diverged"
+        assert ei.value.diverged_t == pytest.approx(float(rec["diverged_t"]), abs=1e-15)
+        return
+    got = port.analyze(rec["x"], rec["y"], rec["r"], idx, workers=4, **kw)
+    # the restatement is compiled with the reference's FMA contraction and
+    # reproduces it bit for bit (non-finite entries in the same places)
+    assert rel_l2(got, rec["out"]) == 0.0
+    fin = np.isfinite(rec["out"])
+    assert np.array_equal(got[fin], rec["out"][fin])
+
+
+def test_port_window_equals_whole(port):
+    rec = CASES["cfg2_like_stride4"]
+    kw = case_kwargs(rec)
+    x, y, r, idx = rec["x"], rec["y"], rec["r"], rec["idx"]
+    whole = port.analyze(x, y, r, idx, workers=4, **kw)
+    d = x.shape[1]
+    parts = []
+    for lo, hi in ((0, 96), (96, 200), (200, d)):
+        sel = (idx >= lo) & (idx < hi)
+        parts.append(port.analyze(x[:, lo:hi], y[sel], r[sel], idx[sel], workers=4, k0=lo,
+                                  d_total=d, **kw))
+    assert np.array_equal(np.concatenate(parts, axis=1), whole)
+
+
+def test_relax_spread_golden(port):
+    s = np.load(ROOT / "tests" / "golden" / "scores.npz")
+    for f, want in zip(s["relax_factors"], s["relax"]):
+        got = port.relax_spread(s["relax_a"], s["x"], float(f))
+        assert rel_l2(got, want) < 1e-14
+
+
+def test_batch_table_matches_reference_stream(port, ref):
+    # proj/src/ensf.cpp:156-167 draws from RngStream(seed, ensf_batch, (cycle<<20)+s)
+    m, j, steps = 50, 10, 7
+    table = port.batch_table(11, 3, m, j, steps)
+    for s in range(steps):
+        u = ref.stream_u64(11, 7, (3 << 20) + s, j)
+        pool = list(range(m))
+        for k in range(j):
+            r = k + int(int(u[k]) % (m - k))
+            pool[k], pool[r] = pool[r], pool[k]
+        assert list(table[s]) == pool[:j]
+
+
+def test_reference_oracle_reproduces_goldens(ref):
+    """oracle/_ref is the generator of the fixtures; this pins that the
+    shipped build (native or portable) still reproduces them bit for bit."""
+    for name in ("cfg1_like_ident_s50", "minibatch10_relax05", "selection_duplicates"):
+        rec = CASES[name]
+        kw = case_kwargs(rec)
+        idx = rec["idx"] if int(rec["obs_kind"]) == 1 else None
+        got = ref.analyze(rec["x"], rec["y"], rec["r"], idx, workers=4, **kw)
+        assert rel_l2(got, rec["out"]) < 1e-13
