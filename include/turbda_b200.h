@@ -108,7 +108,8 @@ void turbda_ensf_params_init(turbda_ensf_params* p);
  * y, r_diag    [obs_dim] fp64
  * obs_idx      [obs_dim] global state indices (index_selection); NULL for identity
  * analysis_out [n_members][d_local] fp64
- * stream       cudaStream_t to run on (device mode); NULL = per-device stream
+ * stream       cudaStream_t to run on; NULL = the legacy default stream in
+ *              device mode, an internal per-device stream in host mode
  */
 int turbda_ensf_analyze(const turbda_ensf_params* p, const double* forecast, const double* y,
                         const double* r_diag, const int64_t* obs_idx, double* analysis_out,
@@ -156,6 +157,13 @@ const char* turbda_build_arch(void);
 
 /* Kernel launches issued by this process since load (evidence counter). */
 uint64_t turbda_launch_count(void);
+
+/* Live timing of the fused analysis kernel: when enabled, every analysis
+ * records CUDA events on its launching stream around the ensf kernel.
+ * turbda_profile_read() returns (and resets) the summed kernel milliseconds
+ * and the number of timed launches since the previous read. */
+void turbda_profile_enable(int on);
+int turbda_profile_read(double* kernel_ms, uint64_t* launches);
 
 #ifdef __cplusplus
 }

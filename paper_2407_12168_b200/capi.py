@@ -83,6 +83,10 @@ def lib() -> C.CDLL:
         L.turbda_abi_version.restype = C.c_int
         L.turbda_build_arch.restype = C.c_char_p
         L.turbda_launch_count.restype = C.c_uint64
+        L.turbda_profile_enable.argtypes = [C.c_int]
+        L.turbda_profile_enable.restype = None
+        L.turbda_profile_read.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+        L.turbda_profile_read.restype = C.c_int
         _lib = L
     return _lib
 
@@ -200,6 +204,17 @@ def device_count() -> int:
 
 def launch_count() -> int:
     return int(lib().turbda_launch_count())
+
+
+def profile_enable(on: bool = True) -> None:
+    lib().turbda_profile_enable(1 if on else 0)
+
+
+def profile_read() -> tuple[float, int]:
+    """(summed fused-kernel ms, timed launches) since the previous read."""
+    ms, n = C.c_double(), C.c_uint64()
+    lib().turbda_profile_read(C.byref(ms), C.byref(n))
+    return float(ms.value), int(n.value)
 
 
 def exported_symbols() -> list[str]:

@@ -26,6 +26,18 @@ namespace {
 
 std::atomic<uint64_t> g_launches{0};
 
+// Optional live timing of the fused analysis kernel (bench.py's roofline):
+// CUDA events recorded on the launching stream around each ensf launch.
+std::atomic<int> g_profile{0};
+std::mutex g_prof_mu;
+struct ProfPair {
+    cudaEvent_t a = nullptr, b = nullptr;
+    int device = 0;
+};
+std::vector<ProfPair> g_prof_pending;
+double g_prof_ms = 0.0;
+uint64_t g_prof_n = 0;
+
 int fail(turbda_status* st, int code, const std::string& msg) {
     if (st) {
         st->code = code;
@@ -214,9 +226,10 @@ int upload_steps(Workspace* w, const turbda_ensf_params* p, cudaStream_t s, turb
         for (size_t s2 = 0; s2 < g.size(); ++s2) {
             const StepTimes& q = g[s2];
             StepF32& o = h[s2];
-            o.na = float(-q.alpha);
-            o.cl = float(log2e / (2.0 * q.beta2));
-            o.kp = float(-q.s2 * q.dt / q.beta2);
+            const double sc = std::sqrt(log2e / (2.0 * q.beta2));
+            o.s = float(sc);
+            o.nas = float(-q.alpha * sc);
+            o.kp = float(-q.s2 * q.dt / (q.beta2 * sc));
             o.kl = float(q.s2 * q.dt * q.damp);
             o.nbdt = float(-q.b * q.dt);
             o.sig = float(q.sig);
@@ -274,7 +287,10 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
     Workspace* w = workspace(device);
     std::lock_guard<std::mutex> lk(w->mu);
     if (int rc = ws_init(w, st)) return rc;
-    cudaStream_t s = user_stream ? user_stream : w->stream;
+    // device mode follows the caller's stream (NULL = the legacy default
+    // stream, where the caller's buffers were most likely produced); host
+    // mode defaults to the workspace stream
+    cudaStream_t s = user_stream ? user_stream : (on_dev ? cudaStreamLegacy : w->stream);
 
     const int m = p->n_members;
     const int64_t dl = win.dl;
@@ -354,7 +370,7 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
 
     const int64_t k0_global = p->k0 + win.k0_local;
     TB_CUDA(launch_obs_prep(dy, dr, didx, obs_n, p->obs_kind, k0_global, dl, w->ab.as<double2>(), s));
-    g_launches += (p->obs_kind == 0) ? 1 : 2;
+    ++g_launches;
 
     KernelArgs a{};
     a.d_total = p->d_total;
@@ -370,16 +386,29 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
     a.cycle_lo = uint32_t(p->cycle);  // entity = (cycle << 32) | i
 
     unsigned long long* dstatus = w->status.as<unsigned long long>();
+    ProfPair prof;
+    if (g_profile.load()) {
+        prof.device = device;
+        TB_CUDA(cudaEventCreate(&prof.a));
+        TB_CUDA(cudaEventCreate(&prof.b));
+        TB_CUDA(cudaEventRecord(prof.a, s));
+    }
     if (fp32) {
         TB_CUDA(launch_ensf_f32(a, dx, w->ab.as<double2>(), w->steps.as<StepF32>(),
                                 w->batches.as<int32_t>(), w->z.as<float>(), dstatus, s));
+        if (prof.a) TB_CUDA(cudaEventRecord(prof.b, s));
         TB_CUDA(launch_relax_f32(w->z.as<float>(), dx, m, dl, p->relax_factor, dout, s));
     } else {
         TB_CUDA(launch_ensf_f64(a, dx, w->ab.as<double2>(), w->steps.as<StepF64>(),
                                 w->batches.as<int32_t>(), w->z.as<double>(), dstatus, s));
+        if (prof.a) TB_CUDA(cudaEventRecord(prof.b, s));
         TB_CUDA(launch_relax_f64(w->z.as<double>(), dx, m, dl, p->relax_factor, dout, s));
     }
     g_launches += 2;
+    if (prof.a) {
+        std::lock_guard<std::mutex> lk2(g_prof_mu);
+        g_prof_pending.push_back(prof);
+    }
     w->last_m = m;
     w->last_steps = p->n_steps;
     w->last_eps = p->eps;
@@ -698,5 +727,30 @@ int turbda_abi_version(void) { return TURBDA_B200_ABI_VERSION; }
 const char* turbda_build_arch(void) { return "sm_100a"; }
 
 uint64_t turbda_launch_count(void) { return g_launches.load(); }
+
+void turbda_profile_enable(int on) {
+    g_profile.store(on ? 1 : 0);
+}
+
+int turbda_profile_read(double* kernel_ms, uint64_t* launches) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (ProfPair& q : g_prof_pending) {
+        cudaSetDevice(q.device);
+        float ms = 0.f;
+        if (cudaEventSynchronize(q.b) == cudaSuccess &&
+            cudaEventElapsedTime(&ms, q.a, q.b) == cudaSuccess) {
+            g_prof_ms += ms;
+            ++g_prof_n;
+        }
+        cudaEventDestroy(q.a);
+        cudaEventDestroy(q.b);
+    }
+    g_prof_pending.clear();
+    if (kernel_ms) *kernel_ms = g_prof_ms;
+    if (launches) *launches = g_prof_n;
+    g_prof_ms = 0.0;
+    g_prof_n = 0;
+    return TURBDA_OK;
+}
 
 }  // extern "C"

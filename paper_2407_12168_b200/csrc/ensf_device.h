@@ -11,13 +11,15 @@ namespace tb200 {
 // Per pseudo-time step coefficients of the fp32 fast kernel (32 B).  All are
 // derived on the host in fp64 from the reference's time grid
 // (proj/src/ensf.cpp:149,183-190) and rounded once.
+// The kernel works with u = s (z - alpha x), s = sqrt(log2(e) / (2 beta^2)),
+// so a softmax exponent is one FFMA2 away: log2 w = min u^2 - u^2.
 struct StepF32 {
-    float na;     // -alpha(t)
-    float cl;     // log2(e) / (2 beta^2)      softmax exponent scale
-    float kp;     // -sigma^2 dt / beta^2      multiplies sum w (z - a x) / sum w
-    float kl;     // sigma^2 dt h(t)           multiplies B - A z (likelihood)
-    float nbdt;   // -b(t) dt                  drift
-    float sig;    // sqrt(sigma^2 dt)          noise amplitude
+    float s;      // sqrt(log2(e) / (2 beta^2))
+    float nas;    // -alpha(t) s
+    float kp;     // -sigma^2 dt / (beta^2 s)   multiplies sum w u / sum w
+    float kl;     // sigma^2 dt h(t)            multiplies B - A z (likelihood)
+    float nbdt;   // -b(t) dt                   drift
+    float sig;    // sqrt(sigma^2 dt)           noise amplitude
     float pad0, pad1;
 };
 

@@ -135,33 +135,35 @@ __global__ void __launch_bounds__(256) ensf_f32_kernel(KernelArgs a, const doubl
 
     for (int s = 0; s < a.n_steps; ++s) {
         const StepF32 c = cs[s];
-        const float2 na2 = f2(c.na);
+        const float2 nas2 = f2(c.nas);
         const int32_t* bt = kMinibatch ? batches + size_t(s) * size_t(a.j_batch) : nullptr;
 
-        // pass 1: per-coordinate smallest squared distance (softmax shift),
-        // proj/src/ensf.cpp:41-50
-        float2 mn[P];
+        // u_j = s (z - alpha x_j): one FFMA2 per member and coordinate pair
+        float2 zs[P], mn[P];
 #pragma unroll
-        for (int p = 0; p < P; ++p) mn[p] = f2(FLT_MAX);
+        for (int p = 0; p < P; ++p) {
+            zs[p] = __fmul2_rn(z[p], f2(c.s));
+            mn[p] = f2(FLT_MAX);
+        }
+        // pass 1: per-coordinate smallest |u| (the softmax shift of
+        // proj/src/ensf.cpp:41-50, taken on |u| so no square is needed)
 #pragma unroll 4
         for (int jj = 0; jj < a.j_batch; ++jj) {
             const int j = kMinibatch ? __ldg(bt + jj) : jj;
             const float2 xv = xs[j * 32 + lane];
 #pragma unroll
             for (int p = 0; p < P; ++p) {
-                const float2 df = __ffma2_rn(na2, xv, z[p]);
-                const float2 d2 = __fmul2_rn(df, df);
-                mn[p].x = fminf(mn[p].x, d2.x);
-                mn[p].y = fminf(mn[p].y, d2.y);
+                const float2 u = __ffma2_rn(nas2, xv, zs[p]);
+                mn[p].x = fminf(mn[p].x, fabsf(u.x));
+                mn[p].y = fminf(mn[p].y, fabsf(u.y));
             }
         }
-        // pass 2: w = 2^{cl (min - d2)}; den = sum w; num = sum w (z - alpha x),
+        // pass 2: w = 2^(min u^2 - u^2); den = sum w; num = sum w u,
         // proj/src/ensf.cpp:51-61 in the cancellation-free form of :62-63
-        const float2 ncl2 = f2(-c.cl);
-        float2 mc[P], den[P], num[P];
+        float2 m2[P], den[P], num[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            mc[p] = __fmul2_rn(mn[p], f2(c.cl));
+            m2[p] = __fmul2_rn(mn[p], mn[p]);
             den[p] = f2(0.f);
             num[p] = f2(0.f);
         }
@@ -171,12 +173,11 @@ __global__ void __launch_bounds__(256) ensf_f32_kernel(KernelArgs a, const doubl
             const float2 xv = xs[j * 32 + lane];
 #pragma unroll
             for (int p = 0; p < P; ++p) {
-                const float2 df = __ffma2_rn(na2, xv, z[p]);
-                const float2 d2 = __fmul2_rn(df, df);
-                const float2 e = __ffma2_rn(d2, ncl2, mc[p]);
+                const float2 u = __ffma2_rn(nas2, xv, zs[p]);
+                const float2 e = __ffma2_rn(make_float2(-u.x, -u.y), u, m2[p]);
                 const float2 w = make_float2(ex2f(e.x), ex2f(e.y));
                 den[p] = __fadd2_rn(den[p], w);
-                num[p] = __ffma2_rn(w, df, num[p]);
+                num[p] = __ffma2_rn(w, u, num[p]);
             }
         }
         // posterior score + Euler-Maruyama, proj/src/ensf.cpp:197-214

@@ -23,12 +23,13 @@ __device__ __forceinline__ PhiloxOut philox_block(uint64_t q, uint32_t e_lo, uin
     uint32_t c0 = uint32_t(q), c1 = uint32_t(q >> 32), c2 = e_lo, c3 = e_hi;
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
-        const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
-        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-        c0 = hi1 ^ c1 ^ k0;
-        c2 = hi0 ^ c3 ^ k1;
-        c1 = lo1;
-        c3 = lo0;
+        // one IMAD.WIDE.U32 per product yields both halves
+        const uint64_t p0 = uint64_t(c0) * 0xD2511F53u;
+        const uint64_t p1 = uint64_t(c2) * 0xCD9E8D57u;
+        c0 = uint32_t(p1 >> 32) ^ c1 ^ k0;
+        c2 = uint32_t(p0 >> 32) ^ c3 ^ k1;
+        c1 = uint32_t(p1);
+        c3 = uint32_t(p0);
         k0 += 0x9E3779B9u;
         k1 += 0xBB67AE85u;
     }

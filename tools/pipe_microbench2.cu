@@ -1,0 +1,65 @@
+// Per-SMSP issue cost of the instructions the EnSF kernel is made of (sm_100a).
+// One CTA per SM, 16 warps (4 per SMSP), independent chains; reports
+// warp-instructions per SMSP-cycle (1.0 = one per clock).
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define ITERS 2048
+#define CH 8
+
+__device__ __forceinline__ float ex2(float x) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+
+template <int OP>
+__global__ void kern(float* out, long long* cyc, float seed) {
+  float a[CH], b[CH]; float2 p[CH]; unsigned u[CH], v[CH];
+  #pragma unroll
+  for (int c = 0; c < CH; ++c) { a[c] = seed * (threadIdx.x + c); b[c] = seed - c; p[c] = make_float2(a[c], b[c]); u[c] = threadIdx.x * 77u + c; v[c] = c * 13u + 1; }
+  const float2 k2 = make_float2(seed * 0.999f, seed * 0.998f), c2 = make_float2(1e-3f, 2e-3f);
+  __syncthreads();
+  long long t0 = clock64();
+  for (int i = 0; i < ITERS; ++i) {
+    #pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (OP == 0) a[c] = fmaf(a[c], b[c], a[(c + 1) % CH]);                 // FFMA 3-reg
+      if (OP == 1) p[c] = __ffma2_rn(p[c], k2, c2);                           // FFMA2
+      if (OP == 2) p[c] = __fadd2_rn(p[c], k2);                               // FADD2
+      if (OP == 3) a[c] = fminf(a[c], b[c] * 0.f + a[(c + 3) % CH]);          // FMNMX (+FFMA)
+      if (OP == 4) a[c] = ex2(a[c]);                                          // MUFU.EX2
+      if (OP == 5) { unsigned long long w = (unsigned long long)u[c] * 0xD2511F53u; u[c] = (unsigned)(w >> 32) ^ v[c]; v[c] = (unsigned)w; } // IMAD.WIDE + LOP
+      if (OP == 6) { u[c] = __umulhi(u[c], 0xD2511F53u) ^ v[c]; v[c] = v[c] * 0xCD9E8D57u; }  // IMAD.HI + IMAD
+      if (OP == 7) { p[c] = __ffma2_rn(p[c], k2, c2); a[c] = ex2(a[c]); }     // FFMA2 + MUFU mix 1:1
+      if (OP == 8) { a[c] = fmaf(a[c], 0.999f, b[c]); }                       // FFMA imm
+      if (OP == 9) { u[c] = u[c] ^ (v[c] >> 3) ^ 0x1234u; v[c] += u[c]; }    // LOP3 + IADD
+      if (OP == 10) { a[c] = __fmul_rn(a[c], b[c]); b[c] = __fadd_rn(b[c], a[(c+1)%CH]); } // FMUL + FADD
+    }
+  }
+  long long t1 = clock64();
+  float s = 0; for (int c = 0; c < CH; ++c) s += a[c] + p[c].x + p[c].y + float(u[c] ^ v[c]);
+  if (s == 1.2345f) out[0] = s;
+  if ((threadIdx.x & 31) == 0) cyc[blockIdx.x * 32 + (threadIdx.x >> 5)] = t1 - t0;
+}
+
+template <int OP>
+void run(const char* name, double instr_per_iter_chain) {
+  int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  float* d; long long* cyc; cudaMalloc(&d, 64); cudaMalloc(&cyc, sizeof(long long) * nsm * 32);
+  for (int warps : {4, 16, 32}) {
+    kern<OP><<<nsm, 32 * warps>>>(d, cyc, 1.0f);
+    cudaDeviceSynchronize();
+    long long* h = new long long[nsm * 32]; cudaMemcpy(h, cyc, sizeof(long long) * nsm * 32, cudaMemcpyDeviceToHost);
+    long long mx = 0; for (int b = 0; b < nsm; ++b) for (int w = 0; w < warps; ++w) mx = h[b*32+w] > mx ? h[b*32+w] : mx;
+    double winstr = double(warps) / 4.0 * ITERS * CH * instr_per_iter_chain;  // per SMSP
+    printf("%-22s warps/SM=%2d  warp-instr per SMSP-clk = %.3f  (%s)\n", name, warps, winstr / mx, cudaGetErrorString(cudaGetLastError()));
+    delete[] h;
+  }
+  cudaFree(d); cudaFree(cyc);
+}
+
+int main() {
+  run<0>("FFMA", 1); run<8>("FFMA-imm", 1); run<1>("FFMA2", 1); run<2>("FADD2", 1);
+  run<3>("FMNMX+FFMA(x0)", 2); run<4>("MUFU.EX2", 1); run<5>("IMAD.WIDE+LOP3(2)", 2);
+  run<6>("IMAD.HI+LOP+IMAD", 3); run<7>("FFMA2+MUFU", 2); run<9>("LOP3+SHF+IADD", 3);
+  run<10>("FMUL+FADD", 2);
+  return 0;
+}
