@@ -79,8 +79,11 @@ struct Workspace {
     std::mutex mu;
     int device = -1;
     cudaStream_t stream = nullptr;
-    DevBuf x, z, ab, steps, batches, status, out, y, r, idx;
+    DevBuf x, z, xt, ab, steps, batches, status, out, y, r, idx;
     unsigned long long* status_host = nullptr;  // pinned
+    std::vector<cudaStream_t> cstreams;         // host-mode chunk pipeline
+    std::vector<cudaEvent_t> ev_chunk;
+    cudaEvent_t ev_ready = nullptr;
     // cached step table / batch table keys
     std::vector<unsigned char> steps_key, batch_key;
     // last analysis (for turbda_ensf_check)
@@ -106,6 +109,7 @@ int ws_init(Workspace* w, turbda_status* st) {
     if (!w->stream) {
         TB_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
         TB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->status_host), 64));
+        TB_CUDA(cudaEventCreateWithFlags(&w->ev_ready, cudaEventDisableTiming));
     }
     return TURBDA_OK;
 }
@@ -272,13 +276,33 @@ int upload_batches(Workspace* w, const turbda_ensf_params* p, int j_batch, cudaS
 }
 
 struct Window {
-    int64_t k0_local;  // offset of this device's slice inside the call's window
+    int64_t k0_local;  // offset of this slice inside the enclosing window
     int64_t dl;        // coordinates in this slice
+    int64_t off() const { return k0_local; }
 };
 
+constexpr int kMaxChunks = 8;
+
+int ws_streams(Workspace* w, int n, turbda_status* st) {
+    while (int(w->cstreams.size()) < n) {
+        cudaStream_t cs;
+        cudaEvent_t ev;
+        TB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        TB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        w->cstreams.push_back(cs);
+        w->ev_chunk.push_back(ev);
+    }
+    return TURBDA_OK;
+}
+
 // Runs one analysis slice on one device.  Host mode: `forecast`/`out` are the
-// call's host arrays with row pitch p->d_local; the slice starts at column
-// win.k0_local.  Device mode: pointers are device pointers of the full window.
+// call's host arrays with row pitch p->d_local (or member rows); the slice
+// starts at column win.k0_local.  The slice is cut into up to kMaxChunks
+// contiguous coordinate chunks, each on its own stream, so the H2D copy of
+// chunk c+1, the kernels of chunk c and the D2H copy of chunk c-1 overlap
+// (chunks are independent: the score is componentwise).  Device mode:
+// pointers are device pointers of the whole window, one pass on the
+// caller's stream.
 int run_slice(const turbda_ensf_params* p, const Window& win, int device, const double* forecast,
               const double* const* frows, const double* y, const double* r, const int64_t* idx,
               double* out, double* const* orows, cudaStream_t user_stream, turbda_status* st) {
@@ -289,7 +313,7 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
     if (int rc = ws_init(w, st)) return rc;
     // device mode follows the caller's stream (NULL = the legacy default
     // stream, where the caller's buffers were most likely produced); host
-    // mode defaults to the workspace stream
+    // mode runs on the workspace streams
     cudaStream_t s = user_stream ? user_stream : (on_dev ? cudaStreamLegacy : w->stream);
 
     const int m = p->n_members;
@@ -302,80 +326,71 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
     if (j_batch != m)
         if (int rc = upload_batches(w, p, j_batch, s, st)) return rc;
 
-    const double* dx;
-    const double *dy, *dr;
-    const int64_t* didx = nullptr;
-    double* dout;
-    int64_t obs_n = p->obs_dim;
-    if (on_dev) {
-        dx = forecast;
-        dy = y;
-        dr = r;
-        didx = idx;
-        dout = out;
-    } else {
-        TB_CUDA(w->x.reserve(sizeof(double) * md));
-        TB_CUDA(w->out.reserve(sizeof(double) * md));
-        // forecast slice [m][k0_local : k0_local + dl] of the host [m][d_local]
-        // array, or of the member rows when the caller keeps them apart
-        if (dl > 0 && m > 0) {
-            if (frows) {
-                for (int j = 0; j < m; ++j)
-                    TB_CUDA(cudaMemcpyAsync(w->x.as<double>() + size_t(j) * size_t(dl),
-                                            frows[j] + win.k0_local, sizeof(double) * size_t(dl),
-                                            cudaMemcpyHostToDevice, s));
-            } else {
-                TB_CUDA(cudaMemcpy2DAsync(w->x.p, sizeof(double) * size_t(dl),
-                                          forecast + win.k0_local,
-                                          sizeof(double) * size_t(p->d_local),
-                                          sizeof(double) * size_t(dl), size_t(m),
-                                          cudaMemcpyHostToDevice, s));
-            }
+    // chunking (host mode): >= 8 MB of forecast per chunk, tile aligned
+    std::vector<Window> chunks;
+    {
+        const int64_t tiles = (dl + 63) / 64;
+        int c = 1;
+        if (!on_dev) {
+            const int64_t bytes = int64_t(md) * int64_t(sizeof(double));
+            c = int(std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, bytes / (8 << 20))));
+            c = int(std::min<int64_t>(c, std::max<int64_t>(tiles, 1)));
         }
-        if (p->obs_kind == 0) {
-            obs_n = dl;
-            TB_CUDA(w->y.reserve(sizeof(double) * size_t(std::max<int64_t>(obs_n, 1))));
-            TB_CUDA(w->r.reserve(sizeof(double) * size_t(std::max<int64_t>(obs_n, 1))));
-            if (obs_n > 0) {
-                TB_CUDA(cudaMemcpyAsync(w->y.p, y + win.k0_local, sizeof(double) * size_t(obs_n),
-                                        cudaMemcpyHostToDevice, s));
-                TB_CUDA(cudaMemcpyAsync(w->r.p, r + win.k0_local, sizeof(double) * size_t(obs_n),
-                                        cudaMemcpyHostToDevice, s));
-            }
-        } else {
-            const size_t nb = size_t(std::max<int64_t>(obs_n, 1));
-            TB_CUDA(w->y.reserve(sizeof(double) * nb));
-            TB_CUDA(w->r.reserve(sizeof(double) * nb));
-            TB_CUDA(w->idx.reserve(sizeof(int64_t) * nb));
-            if (obs_n > 0) {
-                TB_CUDA(cudaMemcpyAsync(w->y.p, y, sizeof(double) * size_t(obs_n),
-                                        cudaMemcpyHostToDevice, s));
-                TB_CUDA(cudaMemcpyAsync(w->r.p, r, sizeof(double) * size_t(obs_n),
-                                        cudaMemcpyHostToDevice, s));
-                TB_CUDA(cudaMemcpyAsync(w->idx.p, idx, sizeof(int64_t) * size_t(obs_n),
-                                        cudaMemcpyHostToDevice, s));
-            }
-            didx = w->idx.as<int64_t>();
+        int64_t start = 0;
+        for (int q = 0; q < c; ++q) {
+            const int64_t end = std::min<int64_t>(dl, (tiles * (q + 1) / c) * 64);
+            chunks.push_back(Window{start, end - start});
+            start = end;
         }
-        dx = w->x.as<double>();
-        dy = w->y.as<double>();
-        dr = w->r.as<double>();
-        dout = w->out.as<double>();
     }
+    const int nc = int(chunks.size());
+    if (int rc = ws_streams(w, nc, st)) return rc;
 
+    // scratch: every chunk owns a disjoint region
+    size_t xt_total = 0;
+    std::vector<size_t> xt_off;
+    for (const Window& c : chunks) {
+        xt_off.push_back(xt_total);
+        xt_total += fp32 ? ensf_f32_scratch_bytes(m, c.dl) : 0;
+    }
     TB_CUDA(w->z.reserve((fp32 ? sizeof(float) : sizeof(double)) * std::max<size_t>(md, 1)));
+    TB_CUDA(w->xt.reserve(std::max<size_t>(xt_total, 1)));
     TB_CUDA(w->ab.reserve(sizeof(double2) * size_t(std::max<int64_t>(dl, 1))));
     TB_CUDA(w->status.reserve(64));
-    TB_CUDA(cudaMemsetAsync(w->status.p, 0xff, sizeof(unsigned long long), s));
+    unsigned long long* dstatus = w->status.as<unsigned long long>();
+    TB_CUDA(cudaMemsetAsync(dstatus, 0xff, sizeof(unsigned long long), s));
 
-    const int64_t k0_global = p->k0 + win.k0_local;
-    TB_CUDA(launch_obs_prep(dy, dr, didx, obs_n, p->obs_kind, k0_global, dl, w->ab.as<double2>(), s));
-    ++g_launches;
+    const double *dx0 = forecast, *dy = y, *dr = r;
+    const int64_t* didx = idx;
+    double* dout0 = out;
+    if (!on_dev) {
+        TB_CUDA(w->x.reserve(sizeof(double) * std::max<size_t>(md, 1)));
+        TB_CUDA(w->out.reserve(sizeof(double) * std::max<size_t>(md, 1)));
+        dx0 = w->x.as<double>();
+        dout0 = w->out.as<double>();
+        const size_t nb = size_t(std::max<int64_t>(p->obs_kind == 0 ? dl : p->obs_dim, 1));
+        TB_CUDA(w->y.reserve(sizeof(double) * nb));
+        TB_CUDA(w->r.reserve(sizeof(double) * nb));
+        dy = w->y.as<double>();
+        dr = w->r.as<double>();
+        if (p->obs_kind == 1) {
+            // selection entries are global: every chunk scans all of them
+            TB_CUDA(w->idx.reserve(sizeof(int64_t) * nb));
+            didx = w->idx.as<int64_t>();
+            if (p->obs_dim > 0) {
+                TB_CUDA(cudaMemcpyAsync(w->y.p, y, sizeof(double) * size_t(p->obs_dim),
+                                        cudaMemcpyHostToDevice, s));
+                TB_CUDA(cudaMemcpyAsync(w->r.p, r, sizeof(double) * size_t(p->obs_dim),
+                                        cudaMemcpyHostToDevice, s));
+                TB_CUDA(cudaMemcpyAsync(w->idx.p, idx, sizeof(int64_t) * size_t(p->obs_dim),
+                                        cudaMemcpyHostToDevice, s));
+            }
+        }
+        TB_CUDA(cudaEventRecord(w->ev_ready, s));
+    }
 
     KernelArgs a{};
     a.d_total = p->d_total;
-    a.k0 = k0_global;
-    a.dl = dl;
     a.m = m;
     a.n_steps = p->n_steps;
     a.j_batch = j_batch;
@@ -385,26 +400,68 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
     a.key1 = uint32_t(key >> 32);
     a.cycle_lo = uint32_t(p->cycle);  // entity = (cycle << 32) | i
 
-    unsigned long long* dstatus = w->status.as<unsigned long long>();
     ProfPair prof;
-    if (g_profile.load()) {
+    if (g_profile.load() && on_dev) {
         prof.device = device;
         TB_CUDA(cudaEventCreate(&prof.a));
         TB_CUDA(cudaEventCreate(&prof.b));
-        TB_CUDA(cudaEventRecord(prof.a, s));
     }
-    if (fp32) {
-        TB_CUDA(launch_ensf_f32(a, dx, w->ab.as<double2>(), w->steps.as<StepF32>(),
-                                w->batches.as<int32_t>(), w->z.as<float>(), dstatus, s));
-        if (prof.a) TB_CUDA(cudaEventRecord(prof.b, s));
-        TB_CUDA(launch_relax_f32(w->z.as<float>(), dx, m, dl, p->relax_factor, dout, s));
-    } else {
-        TB_CUDA(launch_ensf_f64(a, dx, w->ab.as<double2>(), w->steps.as<StepF64>(),
-                                w->batches.as<int32_t>(), w->z.as<double>(), dstatus, s));
-        if (prof.a) TB_CUDA(cudaEventRecord(prof.b, s));
-        TB_CUDA(launch_relax_f64(w->z.as<double>(), dx, m, dl, p->relax_factor, dout, s));
+
+    for (int q = 0; q < nc; ++q) {
+        const Window& c = chunks[size_t(q)];
+        cudaStream_t cs = on_dev ? s : w->cstreams[size_t(q)];
+        const size_t moff = size_t(m) * size_t(c.off());
+        const double* dx = on_dev ? forecast + 0 : dx0 + moff;
+        double* dout = on_dev ? out : dout0 + moff;
+        const int64_t col = win.k0_local + c.k0_local;  // column in the caller's arrays
+        if (!on_dev) {
+            TB_CUDA(cudaStreamWaitEvent(cs, w->ev_ready, 0));
+            if (c.dl > 0 && m > 0) {
+                if (frows) {
+                    for (int j = 0; j < m; ++j)
+                        TB_CUDA(cudaMemcpyAsync(w->x.as<double>() + moff + size_t(j) * size_t(c.dl),
+                                                frows[j] + col, sizeof(double) * size_t(c.dl),
+                                                cudaMemcpyHostToDevice, cs));
+                } else {
+                    TB_CUDA(cudaMemcpy2DAsync(w->x.as<double>() + moff, sizeof(double) * size_t(c.dl),
+                                              forecast + col, sizeof(double) * size_t(p->d_local),
+                                              sizeof(double) * size_t(c.dl), size_t(m),
+                                              cudaMemcpyHostToDevice, cs));
+                }
+            }
+            if (p->obs_kind == 0 && c.dl > 0) {
+                TB_CUDA(cudaMemcpyAsync(w->y.as<double>() + c.k0_local, y + col,
+                                        sizeof(double) * size_t(c.dl), cudaMemcpyHostToDevice, cs));
+                TB_CUDA(cudaMemcpyAsync(w->r.as<double>() + c.k0_local, r + col,
+                                        sizeof(double) * size_t(c.dl), cudaMemcpyHostToDevice, cs));
+            }
+        }
+        const int64_t k0c = p->k0 + col;
+        double2* abc = w->ab.as<double2>() + c.k0_local;
+        const double* yc = p->obs_kind == 0 ? dy + c.k0_local : dy;
+        const double* rc_ = p->obs_kind == 0 ? dr + c.k0_local : dr;
+        const int64_t nobs = p->obs_kind == 0 ? c.dl : p->obs_dim;
+        TB_CUDA(launch_obs_prep(yc, rc_, didx, nobs, p->obs_kind, k0c, c.dl, abc, cs));
+        ++g_launches;
+        a.k0 = k0c;
+        a.dl = c.dl;
+        if (prof.a) TB_CUDA(cudaEventRecord(prof.a, cs));
+        if (fp32) {
+            float* zc = w->z.as<float>() + moff;
+            TB_CUDA(launch_ensf_f32(a, dx, abc, w->steps.as<StepF32>(), w->batches.as<int32_t>(),
+                                    reinterpret_cast<float*>(w->xt.as<unsigned char>() + xt_off[size_t(q)]),
+                                    zc, dstatus, cs));
+            if (prof.b) TB_CUDA(cudaEventRecord(prof.b, cs));
+            TB_CUDA(launch_relax_f32(zc, dx, m, c.dl, p->relax_factor, dout, cs));
+        } else {
+            double* zc = w->z.as<double>() + moff;
+            TB_CUDA(launch_ensf_f64(a, dx, abc, w->steps.as<StepF64>(), w->batches.as<int32_t>(),
+                                    zc, dstatus, cs));
+            if (prof.b) TB_CUDA(cudaEventRecord(prof.b, cs));
+            TB_CUDA(launch_relax_f64(zc, dx, m, c.dl, p->relax_factor, dout, cs));
+        }
+        g_launches += fp32 ? 3 : 2;
     }
-    g_launches += 2;
     if (prof.a) {
         std::lock_guard<std::mutex> lk2(g_prof_mu);
         g_prof_pending.push_back(prof);
@@ -415,20 +472,33 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
 
     if (on_dev && (p->flags & TURBDA_ASYNC)) return TURBDA_OK;
 
-    TB_CUDA(cudaMemcpyAsync(w->status_host, dstatus, sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, s));
-    if (!on_dev && dl > 0 && m > 0) {
-        if (orows) {
-            for (int j = 0; j < m; ++j)
-                TB_CUDA(cudaMemcpyAsync(orows[j] + win.k0_local, dout + size_t(j) * size_t(dl),
-                                        sizeof(double) * size_t(dl), cudaMemcpyDeviceToHost, s));
-        } else {
-            TB_CUDA(cudaMemcpy2DAsync(out + win.k0_local, sizeof(double) * size_t(p->d_local),
-                                      dout, sizeof(double) * size_t(dl),
-                                      sizeof(double) * size_t(dl), size_t(m),
-                                      cudaMemcpyDeviceToHost, s));
+    if (!on_dev) {
+        // results back per chunk, in chunk order (for pageable destinations
+        // each copy returns once its chunk is done; later chunks keep running)
+        for (int q = 0; q < nc; ++q) {
+            const Window& c = chunks[size_t(q)];
+            if (c.dl <= 0 || m <= 0) continue;
+            cudaStream_t cs = w->cstreams[size_t(q)];
+            const size_t moff = size_t(m) * size_t(c.off());
+            const int64_t col = win.k0_local + c.k0_local;
+            if (orows) {
+                for (int j = 0; j < m; ++j)
+                    TB_CUDA(cudaMemcpyAsync(orows[j] + col, dout0 + moff + size_t(j) * size_t(c.dl),
+                                            sizeof(double) * size_t(c.dl), cudaMemcpyDeviceToHost, cs));
+            } else {
+                TB_CUDA(cudaMemcpy2DAsync(out + col, sizeof(double) * size_t(p->d_local),
+                                          dout0 + moff, sizeof(double) * size_t(c.dl),
+                                          sizeof(double) * size_t(c.dl), size_t(m),
+                                          cudaMemcpyDeviceToHost, cs));
+            }
+        }
+        for (int q = 0; q < nc; ++q) {
+            TB_CUDA(cudaEventRecord(w->ev_chunk[size_t(q)], w->cstreams[size_t(q)]));
+            TB_CUDA(cudaStreamWaitEvent(s, w->ev_chunk[size_t(q)], 0));
         }
     }
+    TB_CUDA(cudaMemcpyAsync(w->status_host, dstatus, sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s));
     TB_CUDA(cudaStreamSynchronize(s));
     return diverged(p, *w->status_host, st);
 }

@@ -50,9 +50,12 @@ cudaError_t launch_obs_prep(const double* y, const double* r, const int64_t* idx
                             int64_t obs_dim, int obs_kind, int64_t k0, int64_t dl,
                             double2* ab, cudaStream_t st);
 
-// full fused analysis into z (fp32 or fp64 scratch, [m][dl])
+// full fused analysis into z (fp32 or fp64 scratch, [m][dl]).  The fp32 path
+// first converts (and, without minibatches, sorts per coordinate) the
+// forecast into fp32 tiles `xt` of ensf_f32_scratch_bytes(m, dl) bytes.
+size_t ensf_f32_scratch_bytes(int m, int64_t dl);
 cudaError_t launch_ensf_f32(const KernelArgs& a, const double* x, const double2* ab,
-                            const StepF32* steps, const int32_t* batches, float* z,
+                            const StepF32* steps, const int32_t* batches, float* xt, float* z,
                             unsigned long long* status, cudaStream_t st);
 cudaError_t launch_ensf_f64(const KernelArgs& a, const double* x, const double2* ab,
                             const StepF64* steps, const int32_t* batches, double* z,

@@ -20,6 +20,7 @@
 #include <cfloat>
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 
 #include "ensf_device.h"
 #include "philox.cuh"
@@ -82,16 +83,88 @@ __device__ __forceinline__ double2 load_pair(const double* __restrict__ row, int
 // ---------------------------------------------------------------------------
 // fp32 fast kernel
 // ---------------------------------------------------------------------------
-template <int P, bool kMinibatch>
-__global__ void __launch_bounds__(256) ensf_f32_kernel(KernelArgs a, const double* __restrict__ x,
+
+// 2^e (e <= ~0) on the FMA pipe, to offload part of the softmax from MUFU
+// (FA4-style split): e is rounded to j by the 1.5*2^23 shifter, 2^(e-j) comes
+// from a degree-5 minimax polynomial on [-1/2, 1/2] (max rel. error 2.2e-7,
+// the accuracy class of MUFU.EX2) and j is added into the exponent field.
+// e is clamped at -125 so the exponent never underflows (such weights are
+// < 2^-125 of the largest one and vanish from every sum anyway).
+__device__ __forceinline__ float2 ex2_poly2(float2 e) {
+    e.x = fmaxf(e.x, -125.f);
+    e.y = fmaxf(e.y, -125.f);
+    const float2 t = __fadd2_rn(e, f2(12582912.f));                // 1.5 * 2^23 + j
+    const float2 f = __fadd2_rn(e, __fadd2_rn(f2(12582912.f), make_float2(-t.x, -t.y)));
+    float2 p = __ffma2_rn(f2(0.001330954604782164f), f, f2(0.009673058986663818f));
+    p = __ffma2_rn(p, f, f2(0.055505912750959396f));
+    p = __ffma2_rn(p, f, f2(0.24022164940834045f));
+    p = __ffma2_rn(p, f, f2(0.6931470632553101f));
+    p = __ffma2_rn(p, f, f2(1.0000001192092896f));
+    return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                       __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+
+// Smallest |u_j| = |fma(-alpha s, x_j, s z)| over sorted member columns:
+// u_j falls with x_j (alpha > 0), so the nearest member sits where u changes
+// sign.  All 2P searches of a thread (P particles x the coordinate pair)
+// advance together, so each probe round issues 2P independent LDS and the
+// shared-memory latency overlaps; ceil(log2(J + 1)) rounds replace a pass
+// over all J members.
+template <int P>
+__device__ __forceinline__ void nearest_abs_u(const float* __restrict__ xsf, int lane, int j_n,
+                                              int top, float nas, const float2 (&zs)[P],
+                                              float2 (&mn)[P]) {
+    int pos[P][2];
+#pragma unroll
+    for (int p = 0; p < P; ++p) pos[p][0] = pos[p][1] = 0;  // members with u > 0
+    for (int st = top; st > 0; st >>= 1) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int cand = pos[p][h] + st;
+                const float xv = xsf[(min(cand, j_n) - 1) * 64 + 2 * lane + h];
+                const float zc = h ? zs[p].y : zs[p].x;
+                if (cand <= j_n && fmaf(nas, xv, zc) > 0.f) pos[p][h] = cand;
+            }
+        }
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        float r[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int q = pos[p][h];
+            const float zc = h ? zs[p].y : zs[p].x;
+            const float lo = fabsf(fmaf(nas, xsf[max(q - 1, 0) * 64 + 2 * lane + h], zc));
+            const float hi = fabsf(fmaf(nas, xsf[min(q, j_n - 1) * 64 + 2 * lane + h], zc));
+            r[h] = fminf(q > 0 ? lo : FLT_MAX, q < j_n ? hi : FLT_MAX);
+        }
+        mn[p] = make_float2(r[0], r[1]);
+    }
+}
+
+// NaN sorts last so every column stays a permutation of its members.
+__device__ __forceinline__ float sort_key(float v) { return v != v ? __int_as_float(0x7f800000) : v; }
+
+// kSorted: members of every coordinate are sorted once per analysis (the
+// componentwise score only needs the multiset of member values per
+// coordinate, proj/src/ensf.cpp:43-61), pass 1 becomes a binary search.
+// kPolyEvery: every kPolyEvery-th (member, particle) slot of the unrolled
+// member loop takes its two exponentials from ex2_poly2 instead of MUFU.
+template <int P, bool kMinibatch, bool kSorted, int kPolyEvery, int kMinBlocks = 1>
+__global__ void __launch_bounds__(256, kMinBlocks) ensf_f32_kernel(KernelArgs a, const float* __restrict__ xt,
                                                        const double2* __restrict__ ab,
                                                        const StepF32* __restrict__ steps,
                                                        const int32_t* __restrict__ batches,
                                                        float* __restrict__ z_out,
                                                        unsigned long long* __restrict__ status) {
+    static_assert(!(kMinibatch && kSorted), "minibatches use the two-pass member loop");
+    constexpr int U = 4;  // member-loop unroll
     extern __shared__ float4 smem[];
     StepF32* cs = reinterpret_cast<StepF32*>(smem);
-    float2* xs = reinterpret_cast<float2*>(cs + a.n_steps);  // [m][32]
+    float2* xs = reinterpret_cast<float2*>(cs + a.n_steps);  // [m][32] pairs == [m][64] floats
+    float* xsf = reinterpret_cast<float*>(xs);
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -101,10 +174,12 @@ __global__ void __launch_bounds__(256) ensf_f32_kernel(KernelArgs a, const doubl
     const bool aligned = ((a.dl & 1) == 0);
 
     for (int q = threadIdx.x; q < a.n_steps; q += blockDim.x) cs[q] = steps[q];
-    for (int q = threadIdx.x; q < a.m * 32; q += blockDim.x) {
-        const int j = q >> 5, l = q & 31;
-        const double2 v = load_pair(x + size_t(j) * size_t(a.dl), tile0 + 2 * l, a.dl, aligned);
-        xs[q] = make_float2(float(v.x), float(v.y));
+    {
+        // the tile's members, fp32, [m][64] (sorted per column when kSorted),
+        // laid out contiguously by prep_tiles_kernel: coalesced 16 B loads
+        const float4* src = reinterpret_cast<const float4*>(xt + size_t(blockIdx.x) * size_t(a.m) * kTile);
+        float4* dst = reinterpret_cast<float4*>(xs);
+        for (int q = threadIdx.x; q < a.m * (kTile / 4); q += blockDim.x) dst[q] = __ldg(src + q);
     }
     // likelihood operator for this pair: B - A z with A = sum 1/r, B = sum y/r
     float2 A2 = f2(0.f), B2 = f2(0.f);
@@ -120,6 +195,8 @@ __global__ void __launch_bounds__(256) ensf_f32_kernel(KernelArgs a, const doubl
     }
     const float2 nA2 = make_float2(-A2.x, -A2.y);
     const bool has_y = kl + 1 < a.dl;  // the pair's second coordinate is real
+    int top = 1;
+    while (top * 2 <= a.j_batch) top *= 2;
     __syncthreads();
 
     const int i0 = (blockIdx.y * nwarps + warp) * P;
@@ -147,15 +224,19 @@ __global__ void __launch_bounds__(256) ensf_f32_kernel(KernelArgs a, const doubl
         }
         // pass 1: per-coordinate smallest |u| (the softmax shift of
         // proj/src/ensf.cpp:41-50, taken on |u| so no square is needed)
+        if (kSorted) {
+            nearest_abs_u<P>(xsf, lane, a.j_batch, top, c.nas, zs, mn);
+        } else {
 #pragma unroll 4
-        for (int jj = 0; jj < a.j_batch; ++jj) {
-            const int j = kMinibatch ? __ldg(bt + jj) : jj;
-            const float2 xv = xs[j * 32 + lane];
+            for (int jj = 0; jj < a.j_batch; ++jj) {
+                const int j = kMinibatch ? __ldg(bt + jj) : jj;
+                const float2 xv = xs[j * 32 + lane];
 #pragma unroll
-            for (int p = 0; p < P; ++p) {
-                const float2 u = __ffma2_rn(nas2, xv, zs[p]);
-                mn[p].x = fminf(mn[p].x, fabsf(u.x));
-                mn[p].y = fminf(mn[p].y, fabsf(u.y));
+                for (int p = 0; p < P; ++p) {
+                    const float2 u = __ffma2_rn(nas2, xv, zs[p]);
+                    mn[p].x = fminf(mn[p].x, fabsf(u.x));
+                    mn[p].y = fminf(mn[p].y, fabsf(u.y));
+                }
             }
         }
         // pass 2: w = 2^(min u^2 - u^2); den = sum w; num = sum w u,
@@ -167,8 +248,27 @@ __global__ void __launch_bounds__(256) ensf_f32_kernel(KernelArgs a, const doubl
             den[p] = f2(0.f);
             num[p] = f2(0.f);
         }
-#pragma unroll 4
-        for (int jj = 0; jj < a.j_batch; ++jj) {
+        int jj = 0;
+        for (; jj + U <= a.j_batch; jj += U) {
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) {
+                const int j = kMinibatch ? __ldg(bt + jj + uu) : jj + uu;
+                const float2 xv = xs[j * 32 + lane];
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const float2 u = __ffma2_rn(nas2, xv, zs[p]);
+                    const float2 e = __ffma2_rn(make_float2(-u.x, -u.y), u, m2[p]);
+                    float2 w;
+                    if (kPolyEvery > 0 && (uu * P + p) % kPolyEvery == kPolyEvery - 1)
+                        w = ex2_poly2(e);
+                    else
+                        w = make_float2(ex2f(e.x), ex2f(e.y));
+                    den[p] = __fadd2_rn(den[p], w);
+                    num[p] = __ffma2_rn(w, u, num[p]);
+                }
+            }
+        }
+        for (; jj < a.j_batch; ++jj) {
             const int j = kMinibatch ? __ldg(bt + jj) : jj;
             const float2 xv = xs[j * 32 + lane];
 #pragma unroll
@@ -215,6 +315,41 @@ __global__ void __launch_bounds__(256) ensf_f32_kernel(KernelArgs a, const doubl
         }
         if (bad[p] != INT_MAX && kl < a.dl)
             atomicMin(status, (uint64_t(i) << 32) | uint32_t(bad[p]));
+    }
+}
+
+
+// fp64 forecast [m][dl] -> fp32 tiles [tile][m][64] (zero padded past dl).
+// kSort: each of the 64 columns of a tile sorted ascending (NaN last, ties by
+// member index) by rank counting; the rank of (j, c) is the number of members
+// of column c that order before it, so the output is a permutation.
+template <bool kSort>
+__global__ void prep_tiles_kernel(const double* __restrict__ x, int m, int64_t dl,
+                                  float* __restrict__ xt) {
+    extern __shared__ float col[];  // [m][64] this tile's fp32 values
+    const int64_t tile0 = int64_t(blockIdx.x) * kTile;
+    float* out = xt + size_t(blockIdx.x) * size_t(m) * kTile;
+    for (int q = threadIdx.x; q < m * kTile; q += blockDim.x) {
+        const int j = q / kTile, c = q % kTile;
+        const int64_t k = tile0 + c;
+        const float v = k < dl ? float(x[size_t(j) * size_t(dl) + size_t(k)]) : 0.f;
+        if (kSort)
+            col[q] = v;
+        else
+            out[q] = v;
+    }
+    if (!kSort) return;
+    __syncthreads();
+    for (int q = threadIdx.x; q < m * kTile; q += blockDim.x) {
+        const int j = q / kTile, c = q % kTile;
+        const float v = col[q];
+        const float kv = sort_key(v);
+        int rank = 0;
+        for (int i = 0; i < m; ++i) {
+            const float ki = sort_key(col[i * kTile + c]);
+            rank += (ki < kv) || (ki == kv && i < j);
+        }
+        out[rank * kTile + c] = v;
     }
 }
 
@@ -463,23 +598,39 @@ __global__ void diag_kernel(const double* __restrict__ x, int m, int64_t d,
 
 int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
 
+// fp32 kernel variant (sorted members / MUFU-polynomial split); the default is
+// the fastest measured, TURBDA_F32_VARIANT overrides it for experiments.
+int f32_variant() {
+    static const int v = [] {
+        const char* e = std::getenv("TURBDA_F32_VARIANT");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 template <int P>
-cudaError_t launch_f32_p(const KernelArgs& a, const double* x, const double2* ab,
+cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab,
                          const StepF32* steps, const int32_t* batches, float* z,
-                         unsigned long long* status, cudaStream_t st) {
+                         unsigned long long* status, cudaStream_t st, bool sorted) {
     // warps per CTA: enough to cover the members, at most 8
     const int groups = (a.m + P - 1) / P;
     const int nw = groups < 8 ? groups : 8;
     const dim3 block(32 * nw);
     const dim3 grid(unsigned((a.dl + kTile - 1) / kTile), unsigned((groups + nw - 1) / nw));
     const size_t smem = sizeof(StepF32) * size_t(a.n_steps) + sizeof(float2) * 32 * size_t(a.m);
-    auto kern = a.minibatch ? ensf_f32_kernel<P, true> : ensf_f32_kernel<P, false>;
+    const int variant = f32_variant();
+    auto kern = a.minibatch ? ensf_f32_kernel<P, true, false, 0>
+                : !sorted   ? ensf_f32_kernel<P, false, false, 0>
+                : variant == 1 ? ensf_f32_kernel<P, false, true, 8>
+                : variant == 4 ? ensf_f32_kernel<P, false, true, 0, 4>
+                : variant == 5 ? ensf_f32_kernel<P, false, true, 0, 3>
+                               : ensf_f32_kernel<P, false, true, 0>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(smem));
         if (e != cudaSuccess) return e;
     }
-    kern<<<grid, block, smem, st>>>(a, x, ab, steps, batches, z, status);
+    kern<<<grid, block, smem, st>>>(a, xt, ab, steps, batches, z, status);
     return cudaGetLastError();
 }
 
@@ -519,13 +670,33 @@ cudaError_t launch_obs_prep(const double* y, const double* r, const int64_t* idx
     return cudaGetLastError();
 }
 
+size_t ensf_f32_scratch_bytes(int m, int64_t dl) {
+    return sizeof(float) * size_t(m) * size_t((dl + kTile - 1) / kTile) * kTile;
+}
+
 cudaError_t launch_ensf_f32(const KernelArgs& a, const double* x, const double2* ab,
-                            const StepF32* steps, const int32_t* batches, float* z,
+                            const StepF32* steps, const int32_t* batches, float* xt, float* z,
                             unsigned long long* status, cudaStream_t st) {
     if (a.dl <= 0) return cudaSuccess;
-    if (a.m % 4 == 0) return launch_f32_p<4>(a, x, ab, steps, batches, z, status, st);
-    if (a.m % 2 == 0) return launch_f32_p<2>(a, x, ab, steps, batches, z, status, st);
-    return launch_f32_p<1>(a, x, ab, steps, batches, z, status, st);
+    const unsigned tiles = unsigned((a.dl + kTile - 1) / kTile);
+    const bool sorted = !a.minibatch && f32_variant() != 2;
+    const size_t smem = sizeof(float) * size_t(a.m) * kTile;
+    if (sorted) {
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(prep_tiles_kernel<true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            if (e != cudaSuccess) return e;
+        }
+        prep_tiles_kernel<true><<<tiles, 256, smem, st>>>(x, a.m, a.dl, xt);
+    } else {
+        prep_tiles_kernel<false><<<tiles, 256, 0, st>>>(x, a.m, a.dl, xt);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (a.m % 4 == 0 && f32_variant() != 3)
+        return launch_f32_p<4>(a, xt, ab, steps, batches, z, status, st, sorted);
+    if (a.m % 2 == 0) return launch_f32_p<2>(a, xt, ab, steps, batches, z, status, st, sorted);
+    return launch_f32_p<1>(a, xt, ab, steps, batches, z, status, st, sorted);
 }
 
 cudaError_t launch_ensf_f64(const KernelArgs& a, const double* x, const double2* ab,

@@ -42,7 +42,7 @@ py::array_t<double> ensf_analyze(const darray& members, const turbda::GridSpec& 
                                  std::uint64_t cycle, int n_steps, double relax_factor,
                                  int /*workers*/, int thinning, const std::string& precision,
                                  int device, int device_count, double eps, int minibatch_j,
-                                 double damping_t) {
+                                 double damping_t, py::object out_obj) {
     if (members.ndim() != 2) throw turbda::DimensionError("members must be (M, d)");
     const auto m = members.shape(0);
     const auto d = members.shape(1);
@@ -77,7 +77,17 @@ py::array_t<double> ensf_analyze(const darray& members, const turbda::GridSpec& 
     p.device = device;
     p.device_count = device_count;
 
-    py::array_t<double> out({m, d});
+    // out=: a caller-owned (M, d) float64 C-contiguous array (e.g. pinned
+    // host memory) receives the analysis; otherwise a new array is returned
+    py::array_t<double> out;
+    if (out_obj.is_none()) {
+        out = py::array_t<double>({m, d});
+    } else {
+        out = py::array_t<double>::ensure(out_obj);
+        if (!out || out.ndim() != 2 || out.shape(0) != m || out.shape(1) != d ||
+            !(out.flags() & py::array::c_style) || out.ptr() != out_obj.ptr())
+            throw turbda::DimensionError("out must be a C-contiguous float64 (M, d) array");
+    }
     turbda_status st{};
     int rc;
     {
@@ -111,7 +121,7 @@ PYBIND11_MODULE(_core, mod) {
             py::arg("n_steps") = 100, py::arg("relax_factor") = 1.0, py::arg("workers") = 0,
             py::kw_only(), py::arg("thinning") = 0, py::arg("precision") = "fp32",
             py::arg("device") = -1, py::arg("device_count") = 1, py::arg("eps") = 0.01,
-            py::arg("minibatch_j") = 0, py::arg("damping_t") = 1.0,
+            py::arg("minibatch_j") = 0, py::arg("damping_t") = 1.0, py::arg("out") = py::none(),
             "EnSF analysis of an (M, d) float64 forecast ensemble on the GPU; returns (M, d)");
 
     mod.def("device_count", &turbda_device_count);
