@@ -619,12 +619,12 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
     const dim3 grid(unsigned((a.dl + kTile - 1) / kTile), unsigned((groups + nw - 1) / nw));
     const size_t smem = sizeof(StepF32) * size_t(a.n_steps) + sizeof(float2) * 32 * size_t(a.m);
     const int variant = f32_variant();
-    auto kern = a.minibatch ? ensf_f32_kernel<P, true, false, 0>
-                : !sorted   ? ensf_f32_kernel<P, false, false, 0>
-                : variant == 1 ? ensf_f32_kernel<P, false, true, 8>
-                : variant == 4 ? ensf_f32_kernel<P, false, true, 0, 4>
-                : variant == 5 ? ensf_f32_kernel<P, false, true, 0, 3>
-                               : ensf_f32_kernel<P, false, true, 0>;
+    // 3 CTAs of 256 threads per SM (<= 85 registers): measured best; letting
+    // ptxas take more registers (1 CTA/SM) loses ~20%
+    auto kern = a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3>
+                : !sorted   ? ensf_f32_kernel<P, false, false, 0, 3>
+                : variant == 1 ? ensf_f32_kernel<P, false, true, 8, 3>
+                               : ensf_f32_kernel<P, false, true, 0, 3>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(smem));
