@@ -152,7 +152,8 @@ __device__ __forceinline__ float sort_key(float v) { return v != v ? __int_as_fl
 // coordinate, proj/src/ensf.cpp:43-61), pass 1 becomes a binary search.
 // kPolyEvery: every kPolyEvery-th (member, particle) slot of the unrolled
 // member loop takes its two exponentials from ex2_poly2 instead of MUFU.
-template <int P, bool kMinibatch, bool kSorted, int kPolyEvery, int kMinBlocks = 1>
+template <int P, bool kMinibatch, bool kSorted, int kPolyEvery, int kMinBlocks = 1,
+          bool kGlobalX = false>
 __global__ void __launch_bounds__(256, kMinBlocks) ensf_f32_kernel(KernelArgs a, const float* __restrict__ xt,
                                                        const double2* __restrict__ ab,
                                                        const StepF32* __restrict__ steps,
@@ -160,11 +161,16 @@ __global__ void __launch_bounds__(256, kMinBlocks) ensf_f32_kernel(KernelArgs a,
                                                        float* __restrict__ z_out,
                                                        unsigned long long* __restrict__ status) {
     static_assert(!(kMinibatch && kSorted), "minibatches use the two-pass member loop");
+    static_assert(!(kGlobalX && kSorted), "very large ensembles use the two-pass member loop");
     constexpr int U = 4;  // member-loop unroll
     extern __shared__ float4 smem[];
     StepF32* cs = reinterpret_cast<StepF32*>(smem);
-    float2* xs = reinterpret_cast<float2*>(cs + a.n_steps);  // [m][32] pairs == [m][64] floats
-    float* xsf = reinterpret_cast<float*>(xs);
+    // the tile's members: shared memory, or (ensembles too large for it)
+    // read straight from the fp32 tile in global memory through L1/L2
+    const float2* xs = kGlobalX ? reinterpret_cast<const float2*>(
+                                      xt + size_t(blockIdx.x) * size_t(a.m) * kTile)
+                                : reinterpret_cast<const float2*>(cs + a.n_steps);
+    const float* xsf = reinterpret_cast<const float*>(xs);
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -174,11 +180,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) ensf_f32_kernel(KernelArgs a,
     const bool aligned = ((a.dl & 1) == 0);
 
     for (int q = threadIdx.x; q < a.n_steps; q += blockDim.x) cs[q] = steps[q];
-    {
+    if (!kGlobalX) {
         // the tile's members, fp32, [m][64] (sorted per column when kSorted),
         // laid out contiguously by prep_tiles_kernel: coalesced 16 B loads
         const float4* src = reinterpret_cast<const float4*>(xt + size_t(blockIdx.x) * size_t(a.m) * kTile);
-        float4* dst = reinterpret_cast<float4*>(xs);
+        float4* dst = reinterpret_cast<float4*>(cs + a.n_steps);
         for (int q = threadIdx.x; q < a.m * (kTile / 4); q += blockDim.x) dst[q] = __ldg(src + q);
     }
     // likelihood operator for this pair: B - A z with A = sum 1/r, B = sum y/r
@@ -230,7 +236,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) ensf_f32_kernel(KernelArgs a,
 #pragma unroll 4
             for (int jj = 0; jj < a.j_batch; ++jj) {
                 const int j = kMinibatch ? __ldg(bt + jj) : jj;
-                const float2 xv = xs[j * 32 + lane];
+                const float2 xv = kGlobalX ? __ldg(xs + j * 32 + lane) : xs[j * 32 + lane];
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
                     const float2 u = __ffma2_rn(nas2, xv, zs[p]);
@@ -253,7 +259,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) ensf_f32_kernel(KernelArgs a,
 #pragma unroll
             for (int uu = 0; uu < U; ++uu) {
                 const int j = kMinibatch ? __ldg(bt + jj + uu) : jj + uu;
-                const float2 xv = xs[j * 32 + lane];
+                const float2 xv = kGlobalX ? __ldg(xs + j * 32 + lane) : xs[j * 32 + lane];
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
                     const float2 u = __ffma2_rn(nas2, xv, zs[p]);
@@ -270,7 +276,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) ensf_f32_kernel(KernelArgs a,
         }
         for (; jj < a.j_batch; ++jj) {
             const int j = kMinibatch ? __ldg(bt + jj) : jj;
-            const float2 xv = xs[j * 32 + lane];
+            const float2 xv = kGlobalX ? __ldg(xs + j * 32 + lane) : xs[j * 32 + lane];
 #pragma unroll
             for (int p = 0; p < P; ++p) {
                 const float2 u = __ffma2_rn(nas2, xv, zs[p]);
@@ -598,6 +604,12 @@ __global__ void diag_kernel(const double* __restrict__ x, int m, int64_t d,
 
 int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
 
+// Ensembles whose fp32 tile ([m][64] floats) does not fit next to the step
+// table in shared memory read their members from global memory (L1/L2).
+bool f32_members_global(int m, int n_steps) {
+    return sizeof(StepF32) * size_t(n_steps) + sizeof(float) * 64 * size_t(m) > 200 * 1024;
+}
+
 // fp32 kernel variant (sorted members / MUFU-polynomial split); the default is
 // the fastest measured, TURBDA_F32_VARIANT overrides it for experiments.
 int f32_variant() {
@@ -617,11 +629,15 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
     const int nw = groups < 8 ? groups : 8;
     const dim3 block(32 * nw);
     const dim3 grid(unsigned((a.dl + kTile - 1) / kTile), unsigned((groups + nw - 1) / nw));
-    const size_t smem = sizeof(StepF32) * size_t(a.n_steps) + sizeof(float2) * 32 * size_t(a.m);
+    const bool global_x = f32_members_global(a.m, a.n_steps);
+    const size_t smem = sizeof(StepF32) * size_t(a.n_steps) +
+                        (global_x ? 0 : sizeof(float2) * 32 * size_t(a.m));
     const int variant = f32_variant();
     // 3 CTAs of 256 threads per SM (<= 85 registers): measured best; letting
     // ptxas take more registers (1 CTA/SM) loses ~20%
-    auto kern = a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3>
+    auto kern = global_x ? (a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3, true>
+                                        : ensf_f32_kernel<P, false, false, 0, 3, true>)
+                : a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3>
                 : !sorted   ? ensf_f32_kernel<P, false, false, 0, 3>
                 : variant == 1 ? ensf_f32_kernel<P, false, true, 8, 3>
                                : ensf_f32_kernel<P, false, true, 0, 3>;
@@ -679,7 +695,7 @@ cudaError_t launch_ensf_f32(const KernelArgs& a, const double* x, const double2*
                             unsigned long long* status, cudaStream_t st) {
     if (a.dl <= 0) return cudaSuccess;
     const unsigned tiles = unsigned((a.dl + kTile - 1) / kTile);
-    const bool sorted = !a.minibatch && f32_variant() != 2;
+    const bool sorted = !a.minibatch && f32_variant() != 2 && !f32_members_global(a.m, a.n_steps);
     const size_t smem = sizeof(float) * size_t(a.m) * kTile;
     if (sorted) {
         if (smem > 48 * 1024) {

@@ -88,7 +88,7 @@ def test_cfg2_shape_vs_reference(capi, ref):
 
 def test_large_members_smem_and_global_paths(capi, port):
     """N=200 (> the fp64 shared-memory threshold) and odd N, vs the C oracle."""
-    for m, d in ((200, 256), (33, 130)):
+    for m, d in ((200, 256), (33, 130), (1000, 70), (2000, 2)):
         x, y, _, _ = conditioned_inputs(m, d)
         x = x.astype(np.float32).astype(np.float64)
         want = port.analyze(x, y, n_steps=20)

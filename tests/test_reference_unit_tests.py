@@ -1,0 +1,52 @@
+"""The reference's own hot-path unit tests (proj/tests/test_{ensf,rng,
+ensemble,parallel}.cpp, 38 cases), compiled unmodified against
+include/turbda/*.hpp and linked to libturbda_b200.so (oracle/reftests) -
+the drop-in check for the C++ API.
+
+Against its own implementation the reference passes 35 of the 38; the 3
+failures are defects of the tests: a Philox KAT typo
+(test_rng.cpp:23), a sign error in the shrinkage test (test_ensf.cpp:189-199)
+and the bimodal crossing test, which the reference's Euler-Maruyama misses at
+the default 100 steps (test_ensf.cpp:312-329).  The B200 build must fail
+exactly those three."""
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+BIN = ROOT / "oracle" / "_ref" / "reftests_b200"
+EXPECTED_FAILURES = {
+    "philox4x32 known-answer vectors",
+    "reverse SDE step: zero scores and zero noise shrink toward origin",
+    "analyze pulls a collapsed prior toward a bimodal-side observation",
+}
+
+
+def _run(filt=None):
+    if not BIN.exists():
+        pytest.skip("oracle/_ref/reftests_b200 not built (needs /root/reference at build time)")
+    cmd = [str(BIN)] + ([filt] if filt else [])
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600).stdout
+    failed = set(re.findall(r"^\[FAIL\] (.*) \(", out, re.M))
+    passed = set(re.findall(r"^\[PASS\] (.*) \(", out, re.M))
+    return passed, failed, out
+
+
+def test_host_only_reference_cases():
+    """RNG, parallel_for and the operator/ensemble cases need no GPU."""
+    for filt in ("philox", "splitmix", "stream", "uniform", "normal moments", "distinct",
+                 "parallel_for", "TURBDA_WORKERS", "grid operators", "adjoint",
+                 "operator locations", "observation validation", "ensemble validation"):
+        passed, failed, out = _run(filt)
+        assert passed | failed, filt
+        assert failed <= EXPECTED_FAILURES, out
+
+
+@pytest.mark.gpu
+def test_reference_suite_on_b200():
+    passed, failed, out = _run()
+    print(out[-3000:])
+    assert len(passed) + len(failed) == 38
+    assert failed == EXPECTED_FAILURES, out

@@ -1,0 +1,85 @@
+"""CPU, world size 2 over gloo: the state-dimension sharding used by
+``bench.py --gpus N`` / ``device_count > 1``.  Each rank analyses its own
+coordinate window with the C oracle (noise keyed by the global coordinate);
+the gathered windows must equal the unsharded analysis bit for bit, and no
+collective other than the gather is needed."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _shard_bounds(d, world, rank, align=64):
+    tiles = (d + align - 1) // align
+    lo = min(d, tiles * rank // world * align)
+    hi = min(d, tiles * (rank + 1) // world * align)
+    return lo, hi
+
+
+def _worker(rank, world, port, result):
+    import sys
+    sys.path.insert(0, str(ROOT))
+    from oracle.oracle import PortOracle, throughput_inputs
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    port_o = PortOracle()
+    d, m = 1000, 12
+    x, y, idx = throughput_inputs(m, d, oracle=port_o, stride=3)
+    lo, hi = _shard_bounds(d, world, rank)
+    sel = (idx >= lo) & (idx < hi)
+    part = port_o.analyze(x[:, lo:hi], y[sel], 0.8, idx[sel], n_steps=15, k0=lo, d_total=d,
+                          workers=2)
+    parts = [None] * world
+    dist.all_gather_object(parts, (lo, part))
+    if rank == 0:
+        whole = port_o.analyze(x, y, 0.8, idx, n_steps=15, workers=2)
+        got = np.concatenate([p for _, p in sorted(parts, key=lambda t: t[0])], axis=1)
+        result.put(bool(np.array_equal(got, whole)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_shards_reassemble_bitwise():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs)
+    assert q.get(timeout=5) is True
+
+
+def test_shard_bounds_cover_state():
+    for d in (1, 63, 64, 1000, 131072):
+        for world in (1, 2, 3, 8):
+            b = [_shard_bounds(d, world, r) for r in range(world)]
+            assert b[0][0] == 0 and b[-1][1] == d
+            assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
+
+
+def test_bench_shard_observation_indices():
+    """bench.py's per-rank observation indices are the global every-s-th
+    points that fall into the rank's window."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", ROOT / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    d, stride = 1000, 4
+    for k0 in (0, 1000, 2000, 3000):
+        _, _, idx = bench.make_inputs(d, 2, stride, k0)
+        assert np.array_equal(idx, np.arange(k0, k0 + d)[np.arange(k0, k0 + d) % stride == 0])
