@@ -153,7 +153,7 @@ __device__ __forceinline__ float sort_key(float v) { return v != v ? __int_as_fl
 // kPolyEvery: every kPolyEvery-th (member, particle) slot of the unrolled
 // member loop takes its two exponentials from ex2_poly2 instead of MUFU.
 template <int P, bool kMinibatch, bool kSorted, int kPolyEvery, int kMinBlocks = 1,
-          bool kGlobalX = false>
+          bool kGlobalX = false, bool kStagger = false>
 __global__ void __launch_bounds__(256, kMinBlocks) ensf_f32_kernel(KernelArgs a, const float* __restrict__ xt,
                                                        const double2* __restrict__ ab,
                                                        const StepF32* __restrict__ steps,
@@ -214,6 +214,12 @@ __global__ void __launch_bounds__(256, kMinBlocks) ensf_f32_kernel(KernelArgs a,
     for (int p = 0; p < P; ++p) {
         z[p] = normal_pair_f32(kg, uint32_t(i0 + p), a.cycle_lo, a.key0, a.key1);
         bad[p] = INT_MAX;
+    }
+    if (kStagger) {
+        // Warps of co-resident CTAs run identical step sequences and would
+        // stay phase-locked (all in the MUFU-free search/noise phases at
+        // once).  Spread their start over roughly one pseudo-step.
+        __nanosleep(unsigned((warp * 3 + (blockIdx.x % 3)) * 700));
     }
 
     for (int s = 0; s < a.n_steps; ++s) {
@@ -640,6 +646,8 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
                 : a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3>
                 : !sorted   ? ensf_f32_kernel<P, false, false, 0, 3>
                 : variant == 1 ? ensf_f32_kernel<P, false, true, 8, 3>
+                : variant == 6 ? ensf_f32_kernel<P, false, true, 0, 3, false, true>
+                : variant == 7 ? ensf_f32_kernel<P, false, true, 8, 3, false, true>
                                : ensf_f32_kernel<P, false, true, 0, 3>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -709,9 +717,16 @@ cudaError_t launch_ensf_f32(const KernelArgs& a, const double* x, const double2*
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    if (a.m % 4 == 0 && f32_variant() != 3)
+    // particles per warp: 4 when the grid still fills the GPU (a full wave
+    // is 148 SMs x 24 warps), fewer for small windows so more warps exist
+    const int64_t tiles_n = (a.dl + kTile - 1) / kTile;
+    const auto warps_for = [&](int pp) { return tiles_n * ((a.m + pp - 1) / pp); };
+    const int64_t wave = 148 * 24;
+    // (particles past m in the last warp are computed and discarded)
+    if ((a.m % 4 == 0 || a.m >= 32) && warps_for(4) >= wave)
         return launch_f32_p<4>(a, xt, ab, steps, batches, z, status, st, sorted);
-    if (a.m % 2 == 0) return launch_f32_p<2>(a, xt, ab, steps, batches, z, status, st, sorted);
+    if ((a.m % 2 == 0 || a.m >= 16) && warps_for(2) >= wave / 2)
+        return launch_f32_p<2>(a, xt, ab, steps, batches, z, status, st, sorted);
     return launch_f32_p<1>(a, xt, ab, steps, batches, z, status, st, sorted);
 }
 
