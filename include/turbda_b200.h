@@ -85,7 +85,10 @@ typedef struct turbda_ensf_params {
     int32_t n_members;    /* M: forecast members == analysis particles           */
     int32_t n_steps;      /* EnsfConfig::n_steps (>= 10)                          */
     int32_t minibatch_j;  /* EnsfConfig::minibatch_j (0 = all members)           */
-    int32_t obs_kind;     /* 0 identity (obs_dim == d_local), 1 index_selection  */
+    int32_t obs_kind;     /* 0 identity (obs_dim == d_local), 1 index_selection, */
+                          /* 2 arctan of the full state, 3 arctan of selected   */
+                          /* indices (2/3: h(x) = atan(x), a north-star          */
+                          /* extension without a reference implementation)      */
     double eps;           /* EnsfConfig::eps in (0, 1)                            */
     double damping_t;     /* EnsfConfig::damping_t: h(t) = damping_t - t          */
     double relax_factor;  /* EnsfConfig::relax_factor in [0, 1]                   */

@@ -25,6 +25,13 @@
  * reproduces exactly the reference's values for those coordinates; the noise
  * index uses the global coordinate, n = (s + 1) * d_total + k.
  *
+ * Extension (parity UNPINNED - the reference has no such operator,
+ * proj/include/turbda/observation.hpp:12): obs_kind 2 / 3 apply
+ * h(x) = atan(x) to the full state / selected indices (BASELINE north_star,
+ * configs 1 and 5).  The likelihood line of proj/src/ensf.cpp:197-206 then
+ * reads sc[k] += damp * ((y - atan(z_k)) / r) / (1 + z_k^2) - the gradient
+ * H'(z)^T R^-1 (y - h(z)); everything else is unchanged.
+ *
  * Status codes follow include/turbda_b200.h: 0 ok, 1 config, 2 dimension,
  * 3 sampler diverged.
  */
@@ -209,10 +216,18 @@ static void run_particle(orc_job* jb, int i) {
 
         if (jb->obs_kind == 0) {
             for (int64_t k = 0; k < dl; ++k) sc[k] += damp * ((jb->y[k] - z[k]) / jb->r[k]);
-        } else {
+        } else if (jb->obs_kind == 1) {
             for (int64_t q = 0; q < jb->obs_dim; ++q) {
                 const int64_t k = jb->idx[q] - jb->k0;
                 sc[k] += damp * ((jb->y[q] - z[k]) / jb->r[q]);
+            }
+        } else if (jb->obs_kind == 2) { /* extension: h = atan on every entry */
+            for (int64_t k = 0; k < dl; ++k)
+                sc[k] += damp * (((jb->y[k] - atan(z[k])) / jb->r[k]) / (1.0 + z[k] * z[k]));
+        } else { /* extension: h = atan on selected entries */
+            for (int64_t q = 0; q < jb->obs_dim; ++q) {
+                const int64_t k = jb->idx[q] - jb->k0;
+                sc[k] += damp * (((jb->y[q] - atan(z[k])) / jb->r[q]) / (1.0 + z[k] * z[k]));
             }
         }
 
@@ -296,8 +311,9 @@ int orc_analyze(const double* x, int m, int64_t dl, int64_t k0, int64_t d_total,
         return 1;
     if (m < 1 || dl < 0 || k0 < 0 || k0 + dl > d_total) return 2;
     for (int64_t q = 0; q < obs_dim; ++q) if (!(r[q] > 0.0)) return 1;
-    if (obs_kind == 0 && obs_dim != dl) return 2;
-    if (obs_kind != 0)
+    if (obs_kind < 0 || obs_kind > 3) return 1;
+    if ((obs_kind == 0 || obs_kind == 2) && obs_dim != dl) return 2;
+    if (obs_kind == 1 || obs_kind == 3)
         for (int64_t q = 0; q < obs_dim; ++q)
             if (idx[q] < k0 || idx[q] >= k0 + dl) return 2;
 

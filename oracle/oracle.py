@@ -76,12 +76,12 @@ def host_cores() -> int:
         return os.cpu_count() or 1
 
 
-def _obs_arrays(d, y, r, idx):
+def _obs_arrays(d, y, r, idx, arctan=False):
     y = np.ascontiguousarray(y, dtype=np.float64)
     r = np.broadcast_to(np.asarray(r, dtype=np.float64), y.shape).copy()
     if idx is None:
-        return y, r, np.zeros(1, np.int64), 0
-    return y, r, np.ascontiguousarray(idx, dtype=np.int64), 1
+        return y, r, np.zeros(1, np.int64), 2 if arctan else 0
+    return y, r, np.ascontiguousarray(idx, dtype=np.int64), 3 if arctan else 1
 
 
 class RefOracle:
@@ -248,12 +248,13 @@ class PortOracle:
 
     def analyze(self, members, y, r=1.0, idx=None, *, n_steps=100, eps=0.01, minibatch_j=0,
                 damping_t=1.0, relax_factor=1.0, seed=7, cycle=1, workers=0, k0=0,
-                d_total=None):
-        """``members`` is the [m][dl] window starting at global coordinate k0."""
+                d_total=None, arctan=False):
+        """``members`` is the [m][dl] window starting at global coordinate k0.
+        ``arctan=True``: h(x) = atan(x) (extension, parity unpinned)."""
         x = np.ascontiguousarray(members, dtype=np.float64)
         m, dl = x.shape
         d_total = dl if d_total is None else d_total
-        y, r, idx_a, kind = _obs_arrays(dl, y, r, idx)
+        y, r, idx_a, kind = _obs_arrays(dl, y, r, idx, arctan)
         out = np.empty_like(x)
         div_t = C.c_double(float("nan"))
         workers = workers if workers > 0 else host_cores()

@@ -138,7 +138,7 @@ def check(device: int, p: EnsfParams) -> Status:
 
 def analyze_host(members, y, r=1.0, idx=None, *, n_steps=100, eps=0.01, minibatch_j=0,
                  damping_t=1.0, relax_factor=1.0, seed=7, cycle=1, precision=FP32, device=-1,
-                 device_count=1, k0=0, d_total=None):
+                 device_count=1, k0=0, d_total=None, arctan=False):
     """numpy-in / numpy-out analysis over the window [k0, k0 + d) of a state
     of dimension d_total (defaults to the whole state)."""
     x = np.ascontiguousarray(members, dtype=np.float64)
@@ -148,7 +148,8 @@ def analyze_host(members, y, r=1.0, idx=None, *, n_steps=100, eps=0.01, minibatc
     ix = None if idx is None else np.ascontiguousarray(idx, dtype=np.int64)
     p = params(d_total=d if d_total is None else d_total, k0=k0, d_local=d, obs_dim=y.size,
                n_members=m, n_steps=n_steps, minibatch_j=minibatch_j,
-               obs_kind=0 if idx is None else 1, eps=eps, damping_t=damping_t,
+               obs_kind=(0 if idx is None else 1) + (2 if arctan else 0), eps=eps,
+               damping_t=damping_t,
                relax_factor=relax_factor, seed=seed, cycle=cycle, precision=precision,
                device=device, device_count=device_count)
     out = np.empty_like(x)
@@ -157,7 +158,7 @@ def analyze_host(members, y, r=1.0, idx=None, *, n_steps=100, eps=0.01, minibatc
 
 
 def score(z, t, members, batch=None, eps=0.01, y=None, r=None, idx=None, damping_t=1.0,
-          device=-1):
+          device=-1, arctan=False):
     z = np.ascontiguousarray(z, np.float64)
     x = np.ascontiguousarray(members, np.float64)
     b = None if batch is None else np.ascontiguousarray(batch, np.int32)
@@ -172,7 +173,8 @@ def score(z, t, members, batch=None, eps=0.01, y=None, r=None, idx=None, damping
     st = Status()
     code = lib().turbda_score(_ptr(z), z.size, t, _ptr(x), x.shape[0], _ptr(b),
                               0 if b is None else b.size, eps, _ptr(yy), _ptr(rr), _ptr(ii),
-                              nobs, 0 if idx is None else 1, damping_t, _ptr(out), device,
+                              nobs, (0 if idx is None else 1) + (2 if arctan else 0), damping_t,
+                              _ptr(out), device,
                               C.byref(st))
     _check(code, st)
     return out

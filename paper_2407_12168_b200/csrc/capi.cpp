@@ -173,10 +173,10 @@ int validate(const turbda_ensf_params* p, turbda_status* st) {
     if (p->d_local < 0 || p->k0 < 0 || p->d_total < p->k0 + p->d_local)
         return fail(st, TURBDA_DIMENSION, "analyze: window outside the state");
     // Observation::validate length check, include/turbda/observation.hpp:49-55
-    if (p->obs_kind == 0 && p->obs_dim != p->d_local)
-        return fail(st, TURBDA_DIMENSION, "observation: length mismatch");
-    if (p->obs_kind != 0 && p->obs_kind != 1)
+    if (p->obs_kind < 0 || p->obs_kind > 3)
         return fail(st, TURBDA_CONFIG, "observation: unsupported operator kind");
+    if (obs_dense(p->obs_kind) && p->obs_dim != p->d_local)
+        return fail(st, TURBDA_DIMENSION, "observation: length mismatch");
     if (p->obs_dim < 0) return fail(st, TURBDA_DIMENSION, "observation: length mismatch");
     // EnsfConfig::validate, include/turbda/ensf.hpp:29-37
     if (!(p->eps > 0.0 && p->eps < 1.0)) return fail(st, TURBDA_CONFIG, "ensf: eps must lie in (0, 1)");
@@ -194,7 +194,7 @@ int validate_host_obs(const turbda_ensf_params* p, const double* r, const int64_
                       turbda_status* st) {
     for (int64_t q = 0; q < p->obs_dim; ++q)
         if (!(r[q] > 0.0)) return fail(st, TURBDA_CONFIG, "observation: r_diag > 0");
-    if (p->obs_kind == 1)
+    if (!obs_dense(p->obs_kind))
         for (int64_t q = 0; q < p->obs_dim; ++q)
             if (idx[q] < 0 || idx[q] >= p->d_total)
                 return fail(st, TURBDA_DIMENSION, "observation: index outside the state");
@@ -368,12 +368,12 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
         TB_CUDA(w->out.reserve(sizeof(double) * std::max<size_t>(md, 1)));
         dx0 = w->x.as<double>();
         dout0 = w->out.as<double>();
-        const size_t nb = size_t(std::max<int64_t>(p->obs_kind == 0 ? dl : p->obs_dim, 1));
+        const size_t nb = size_t(std::max<int64_t>(obs_dense(p->obs_kind) ? dl : p->obs_dim, 1));
         TB_CUDA(w->y.reserve(sizeof(double) * nb));
         TB_CUDA(w->r.reserve(sizeof(double) * nb));
         dy = w->y.as<double>();
         dr = w->r.as<double>();
-        if (p->obs_kind == 1) {
+        if (!obs_dense(p->obs_kind)) {
             // selection entries are global: every chunk scans all of them
             TB_CUDA(w->idx.reserve(sizeof(int64_t) * nb));
             didx = w->idx.as<int64_t>();
@@ -399,6 +399,7 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
     a.key0 = uint32_t(key);
     a.key1 = uint32_t(key >> 32);
     a.cycle_lo = uint32_t(p->cycle);  // entity = (cycle << 32) | i
+    a.obs_atan = obs_arctan(p->obs_kind) ? 1 : 0;
 
     ProfPair prof;
     if (g_profile.load() && on_dev) {
@@ -429,7 +430,7 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
                                               cudaMemcpyHostToDevice, cs));
                 }
             }
-            if (p->obs_kind == 0 && c.dl > 0) {
+            if (obs_dense(p->obs_kind) && c.dl > 0) {
                 TB_CUDA(cudaMemcpyAsync(w->y.as<double>() + c.k0_local, y + col,
                                         sizeof(double) * size_t(c.dl), cudaMemcpyHostToDevice, cs));
                 TB_CUDA(cudaMemcpyAsync(w->r.as<double>() + c.k0_local, r + col,
@@ -438,9 +439,10 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
         }
         const int64_t k0c = p->k0 + col;
         double2* abc = w->ab.as<double2>() + c.k0_local;
-        const double* yc = p->obs_kind == 0 ? dy + c.k0_local : dy;
-        const double* rc_ = p->obs_kind == 0 ? dr + c.k0_local : dr;
-        const int64_t nobs = p->obs_kind == 0 ? c.dl : p->obs_dim;
+        const bool dense = obs_dense(p->obs_kind);
+        const double* yc = dense ? dy + c.k0_local : dy;
+        const double* rc_ = dense ? dr + c.k0_local : dr;
+        const int64_t nobs = dense ? c.dl : p->obs_dim;
         TB_CUDA(launch_obs_prep(yc, rc_, didx, nobs, p->obs_kind, k0c, c.dl, abc, cs));
         ++g_launches;
         a.k0 = k0c;
@@ -694,11 +696,13 @@ int turbda_score(const double* z, int64_t d, double t, const double* forecast, i
             if (batch[q] < 0 || batch[q] >= m)
                 return fail(st, TURBDA_DIMENSION, "prior_score: batch index out of range");
     if (y) {
-        if ((obs_kind == 0 && obs_dim != d) || obs_dim < 0)
+        if (obs_kind < 0 || obs_kind > 3)
+            return fail(st, TURBDA_CONFIG, "observation: unsupported operator kind");
+        if ((obs_dense(obs_kind) && obs_dim != d) || obs_dim < 0)
             return fail(st, TURBDA_DIMENSION, "likelihood_score: dimension mismatch");
         for (int64_t q = 0; q < obs_dim; ++q)
             if (!(r_diag[q] > 0.0)) return fail(st, TURBDA_CONFIG, "observation: r_diag > 0");
-        if (obs_kind == 1)
+        if (!obs_dense(obs_kind))
             for (int64_t q = 0; q < obs_dim; ++q)
                 if (obs_idx[q] < 0 || obs_idx[q] >= d)
                     return fail(st, TURBDA_DIMENSION, "observation: index outside the state");
@@ -733,7 +737,7 @@ int turbda_score(const double* z, int64_t d, double t, const double* forecast, i
         if (obs_dim > 0) {
             TB_CUDA(cudaMemcpyAsync(w->y.p, y, sizeof(double) * size_t(obs_dim), cudaMemcpyHostToDevice, s));
             TB_CUDA(cudaMemcpyAsync(w->r.p, r_diag, sizeof(double) * size_t(obs_dim), cudaMemcpyHostToDevice, s));
-            if (obs_kind == 1)
+            if (!obs_dense(obs_kind))
                 TB_CUDA(cudaMemcpyAsync(w->idx.p, obs_idx, sizeof(int64_t) * size_t(obs_dim),
                                         cudaMemcpyHostToDevice, s));
         }
@@ -746,7 +750,7 @@ int turbda_score(const double* z, int64_t d, double t, const double* forecast, i
     // NoiseSchedule::alpha / beta2, include/turbda/ensf.hpp:15-20
     TB_CUDA(launch_score_f64(w->z.as<double>(), w->x.as<double>(), m, d,
                              batch ? w->batches.as<int32_t>() : nullptr, nb, 1.0 - t, t, dab, damp,
-                             w->out.as<double>(), s));
+                             obs_arctan(obs_kind) ? 1 : 0, w->out.as<double>(), s));
     ++g_launches;
     TB_CUDA(cudaMemcpyAsync(out, w->out.p, sizeof(double) * size_t(d), cudaMemcpyDeviceToHost, s));
     TB_CUDA(cudaStreamSynchronize(s));

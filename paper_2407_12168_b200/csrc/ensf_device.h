@@ -39,8 +39,12 @@ struct KernelArgs {
     int32_t minibatch; // 1 when `batches` holds a [n_steps][j_batch] table
     uint32_t key0, key1;  // Philox key of the ensf_particles stream
     uint32_t cycle_lo;    // entity = (cycle << 32) | i  ->  hi word
-    int32_t pad;
+    int32_t obs_atan;     // 1: h(x) = atan(x) (obs kinds 2, 3), 0: linear
 };
+
+// observation operator kinds of the C-ABI (include/turbda_b200.h)
+inline bool obs_dense(int kind) { return kind == 0 || kind == 2; }
+inline bool obs_arctan(int kind) { return kind == 2 || kind == 3; }
 
 // Divergence word: min over ((particle << 32) | step); ~0 = none.
 constexpr unsigned long long kNoDivergence = ~0ull;
@@ -70,7 +74,8 @@ cudaError_t launch_relax_f64(const double* z, const double* x, int m, int64_t dl
 // single-vector score (prior_score / posterior_score API), fp64 faithful
 cudaError_t launch_score_f64(const double* z, const double* x, int m, int64_t d,
                              const int32_t* batch, int nbatch, double alpha, double beta2,
-                             const double2* ab, double damp, double* out, cudaStream_t st);
+                             const double2* ab, double damp, int obs_atan, double* out,
+                             cudaStream_t st);
 
 // rmse / spread partial sums: out[0] = sum (mean - truth)^2, out[1] = sum dev^2
 cudaError_t launch_diag(const double* x, int m, int64_t d, const double* truth, double* out,

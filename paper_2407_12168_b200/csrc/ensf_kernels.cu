@@ -331,7 +331,14 @@ __global__ void __launch_bounds__(kProducer ? 256 + 32 * kProducerWarps : 256, k
         for (int p = 0; p < P; ++p) {
             const float2 q = make_float2(__fdividef(num[p].x, den[p].x),
                                          __fdividef(num[p].y, den[p].y));
-            const float2 lik = __ffma2_rn(nA2, z[p], B2);
+            float2 lik;
+            if (a.obs_atan) {
+                // h(z) = atan(z): H'^T R^-1 (y - h) = (B - A atan z) / (1 + z^2)
+                lik.x = fmaf(nA2.x, atanf(z[p].x), B2.x) / fmaf(z[p].x, z[p].x, 1.f);
+                lik.y = fmaf(nA2.y, atanf(z[p].y), B2.y) / fmaf(z[p].y, z[p].y, 1.f);
+            } else {
+                lik = __ffma2_rn(nA2, z[p], B2);
+            }
             const float2 xi = kProducer ? xin[p * 32]
                                         : normal_pair_f32(n0, uint32_t(i0 + p), a.cycle_lo,
                                                           a.key0, a.key1);
@@ -498,8 +505,13 @@ __global__ void __launch_bounds__(128) ensf_f64_kernel(KernelArgs a, const doubl
         for (int p = 0; p < P; ++p) {
             double scx = -(zx[p] - c.alpha * nx[p] / ex[p]) / c.beta2;
             double scy = -(zy[p] - c.alpha * ny[p] / ey[p]) / c.beta2;
-            scx += c.damp * (B.x - A.x * zx[p]);
-            scy += c.damp * (B.y - A.y * zy[p]);
+            if (a.obs_atan) {
+                scx += c.damp * ((B.x - A.x * atan(zx[p])) / (1.0 + zx[p] * zx[p]));
+                scy += c.damp * ((B.y - A.y * atan(zy[p])) / (1.0 + zy[p] * zy[p]));
+            } else {
+                scx += c.damp * (B.x - A.x * zx[p]);
+                scy += c.damp * (B.y - A.y * zy[p]);
+            }
             const double2 xi = normal_pair_f64(n0, uint32_t(i0 + p), a.cycle_lo, a.key0, a.key1);
             zx[p] += -(c.b * zx[p] - c.s2 * scx) * c.dt + c.sig * xi.x;
             zy[p] += -(c.b * zy[p] - c.s2 * scy) * c.dt + c.sig * xi.y;
@@ -590,7 +602,7 @@ __global__ void obs_select_kernel(const double* __restrict__ y, const double* __
 __global__ void score_kernel(const double* __restrict__ z, const double* __restrict__ x, int m,
                              int64_t d, const int32_t* __restrict__ batch, int nbatch,
                              double alpha, double beta2, const double2* __restrict__ ab,
-                             double damp, double* __restrict__ out) {
+                             double damp, int obs_atan, double* __restrict__ out) {
     const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k >= d) return;
     const double inv2b = 1.0 / (2.0 * beta2);
@@ -612,7 +624,9 @@ __global__ void score_kernel(const double* __restrict__ z, const double* __restr
         num += w * xv;
     }
     double s = -(zk - alpha * num / den) / beta2;
-    if (ab) s += damp * (ab[k].y - ab[k].x * zk);
+    if (ab)
+        s += obs_atan ? damp * ((ab[k].y - ab[k].x * atan(zk)) / (1.0 + zk * zk))
+                      : damp * (ab[k].y - ab[k].x * zk);
     out[k] = s;
 }
 
@@ -723,7 +737,7 @@ cudaError_t launch_obs_prep(const double* y, const double* r, const int64_t* idx
                             int64_t obs_dim, int obs_kind, int64_t k0, int64_t dl, double2* ab,
                             cudaStream_t st) {
     if (dl <= 0) return cudaSuccess;
-    if (obs_kind == 0) {
+    if (obs_dense(obs_kind)) {
         obs_identity_kernel<<<blocks_for(dl, 256), 256, 0, st>>>(y, r, dl, ab);
         return cudaGetLastError();
     }
@@ -797,10 +811,11 @@ cudaError_t launch_relax_f64(const double* z, const double* x, int m, int64_t dl
 
 cudaError_t launch_score_f64(const double* z, const double* x, int m, int64_t d,
                              const int32_t* batch, int nbatch, double alpha, double beta2,
-                             const double2* ab, double damp, double* out, cudaStream_t st) {
+                             const double2* ab, double damp, int obs_atan, double* out,
+                             cudaStream_t st) {
     if (d <= 0) return cudaSuccess;
     score_kernel<<<blocks_for(d, 128), 128, 0, st>>>(z, x, m, d, batch, nbatch, alpha, beta2, ab,
-                                                      damp, out);
+                                                      damp, obs_atan, out);
     return cudaGetLastError();
 }
 

@@ -42,7 +42,8 @@ py::array_t<double> ensf_analyze(const darray& members, const turbda::GridSpec& 
                                  std::uint64_t cycle, int n_steps, double relax_factor,
                                  int /*workers*/, int thinning, const std::string& precision,
                                  int device, int device_count, double eps, int minibatch_j,
-                                 double damping_t, py::object out_obj) {
+                                 double damping_t, const std::string& obs_operator,
+                                 py::object out_obj) {
     if (members.ndim() != 2) throw turbda::DimensionError("members must be (M, d)");
     const auto m = members.shape(0);
     const auto d = members.shape(1);
@@ -67,7 +68,9 @@ py::array_t<double> ensf_analyze(const darray& members, const turbda::GridSpec& 
     p.n_members = int32_t(m);
     p.n_steps = n_steps;
     p.minibatch_j = minibatch_j;
-    p.obs_kind = thinning > 1 ? 1 : 0;
+    if (obs_operator != "linear" && obs_operator != "arctan")
+        throw turbda::ConfigError("obs_operator must be 'linear' or 'arctan'");
+    p.obs_kind = (thinning > 1 ? 1 : 0) + (obs_operator == "arctan" ? 2 : 0);
     p.eps = eps;
     p.damping_t = damping_t;
     p.relax_factor = relax_factor;
@@ -121,7 +124,8 @@ PYBIND11_MODULE(_core, mod) {
             py::arg("n_steps") = 100, py::arg("relax_factor") = 1.0, py::arg("workers") = 0,
             py::kw_only(), py::arg("thinning") = 0, py::arg("precision") = "fp32",
             py::arg("device") = -1, py::arg("device_count") = 1, py::arg("eps") = 0.01,
-            py::arg("minibatch_j") = 0, py::arg("damping_t") = 1.0, py::arg("out") = py::none(),
+            py::arg("minibatch_j") = 0, py::arg("damping_t") = 1.0,
+            py::arg("obs_operator") = "linear", py::arg("out") = py::none(),
             "EnSF analysis of an (M, d) float64 forecast ensemble on the GPU; returns (M, d)");
 
     mod.def("device_count", &turbda_device_count);

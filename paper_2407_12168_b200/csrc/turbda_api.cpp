@@ -45,10 +45,21 @@ struct FlatObs {
     int kind = 0;
 };
 
+// C-ABI operator kind: 0 identity, 1 index_selection, 2 arctan, 3 arctan_selection
+int abi_kind(ObsOperatorKind k) {
+    switch (k) {
+        case ObsOperatorKind::identity: return 0;
+        case ObsOperatorKind::index_selection: return 1;
+        case ObsOperatorKind::arctan: return 2;
+        case ObsOperatorKind::arctan_selection: return 3;
+    }
+    return 0;
+}
+
 FlatObs flatten_obs(const Observation& obs) {
     FlatObs f;
-    f.kind = obs.op.kind == ObsOperatorKind::identity ? 0 : 1;
-    if (f.kind == 1) f.idx.assign(obs.op.indices.begin(), obs.op.indices.end());
+    f.kind = abi_kind(obs.op.kind);
+    if (!is_dense(obs.op.kind)) f.idx.assign(obs.op.indices.begin(), obs.op.indices.end());
     return f;
 }
 
@@ -176,16 +187,23 @@ double spread(const Ensemble& ens) {
 // -------------------------------------------------------- observation -----
 std::vector<double> apply_operator(const ObsOperator& op, const std::vector<double>& state) {
     if (state.size() != op.state_dim) throw DimensionError("apply_operator: state dimension mismatch");
-    if (op.kind == ObsOperatorKind::identity) return state;
     std::vector<double> out;
-    out.reserve(op.indices.size());
-    for (const std::size_t k : op.indices) out.push_back(state[k]);
+    if (is_dense(op.kind)) {
+        out = state;
+    } else {
+        out.reserve(op.indices.size());
+        for (const std::size_t k : op.indices) out.push_back(state[k]);
+    }
+    if (is_arctan(op.kind))
+        for (double& v : out) v = std::atan(v);
     return out;
 }
 
+// scatter pattern of the operator (for the arctan kinds: of its linearisation;
+// the derivative factor 1/(1+x^2) is applied by likelihood_score)
 std::vector<double> adjoint_scatter(const ObsOperator& op, const std::vector<double>& w) {
     if (w.size() != op.obs_dim()) throw DimensionError("adjoint_scatter: obs dimension mismatch");
-    if (op.kind == ObsOperatorKind::identity) return w;
+    if (is_dense(op.kind)) return w;
     std::vector<double> out(op.state_dim, 0.0);
     for (std::size_t q = 0; q < op.indices.size(); ++q) out[op.indices[q]] += w[q];
     return out;
@@ -202,6 +220,12 @@ ObsOperator make_grid_operator(const GridSpec& grid, int thinning_stride) {
     return op;
 }
 
+ObsOperator make_arctan_operator(const GridSpec& grid, int thinning_stride) {
+    ObsOperator op = make_grid_operator(grid, thinning_stride);
+    op.kind = thinning_stride > 1 ? ObsOperatorKind::arctan_selection : ObsOperatorKind::arctan;
+    return op;
+}
+
 std::vector<std::array<double, 2>> operator_locations(const GridSpec& grid, const ObsOperator& op) {
     const std::size_t plane = std::size_t(grid.ny) * std::size_t(grid.nx);
     const auto at = [&](std::size_t flat) {
@@ -210,7 +234,7 @@ std::vector<std::array<double, 2>> operator_locations(const GridSpec& grid, cons
                                      double(h / std::size_t(grid.nx))};
     };
     std::vector<std::array<double, 2>> out;
-    if (op.kind == ObsOperatorKind::identity) {
+    if (is_dense(op.kind)) {
         out.reserve(op.state_dim);
         for (std::size_t k = 0; k < op.state_dim; ++k) out.push_back(at(k));
     } else {
@@ -283,6 +307,12 @@ std::vector<double> likelihood_score(const std::vector<double>& z, const Observa
     const std::vector<double> hz = apply_operator(obs.op, z);
     std::vector<double> innov(hz.size());
     for (std::size_t q = 0; q < hz.size(); ++q) innov[q] = (obs.y[q] - hz[q]) / obs.r_diag[q];
+    if (is_arctan(obs.op.kind)) {  // chain rule: d atan(x)/dx = 1 / (1 + x^2)
+        for (std::size_t q = 0; q < innov.size(); ++q) {
+            const double x = is_dense(obs.op.kind) ? z[q] : z[obs.op.indices[q]];
+            innov[q] /= 1.0 + x * x;
+        }
+    }
     return adjoint_scatter(obs.op, innov);
 }
 
@@ -330,7 +360,7 @@ Ensemble analyze(const Ensemble& forecast, const Observation& obs, const EnsfCon
     const std::size_t d = forecast.dim();
     if (obs.op.state_dim != d) throw DimensionError("analyze: observation operator dimension");
     for (const std::size_t k : obs.op.indices)
-        if (obs.op.kind == ObsOperatorKind::index_selection && k >= d)
+        if (!is_dense(obs.op.kind) && k >= d)
             throw DimensionError("analyze: observation index outside the state");
 
     turbda_ensf_params p;
@@ -342,7 +372,7 @@ Ensemble analyze(const Ensemble& forecast, const Observation& obs, const EnsfCon
     p.n_members = forecast.size();
     p.n_steps = cfg.n_steps;
     p.minibatch_j = cfg.minibatch_j;
-    p.obs_kind = obs.op.kind == ObsOperatorKind::identity ? 0 : 1;
+    p.obs_kind = abi_kind(obs.op.kind);
     p.eps = cfg.eps;
     p.damping_t = cfg.damping_t;
     p.relax_factor = cfg.relax_factor;

@@ -210,3 +210,34 @@ def test_cfg2_full_size_properties(capi):
     lo = capi.analyze_host(x[:, :half], y[sel], 1.0, idx[sel], k0=0, d_total=131072)
     hi = capi.analyze_host(x[:, half:], y[~sel], 1.0, idx[~sel], k0=half, d_total=131072)
     assert np.array_equal(np.concatenate([lo, hi], axis=1), a32)
+
+
+# --- extension: arctan observation operator (north_star, configs 1 and 5) ---
+# No reference implementation exists (proj/include/turbda/observation.hpp:12
+# has identity and index_selection only): the oracle is the C restatement
+# with the likelihood line changed (oracle/ensf_oracle.c), parity UNPINNED.
+
+@pytest.mark.parametrize("stride", [1, 4])
+def test_arctan_operator_vs_port(capi, port, stride):
+    x, _, idx, truth = conditioned_inputs(20, 2048, stride=stride)
+    x = x.astype(np.float32).astype(np.float64)
+    ht = truth if idx is None else truth[idx]
+    y = (np.arctan(ht) + 0.1 * np.cos(np.arange(ht.size))).astype(np.float32).astype(np.float64)
+    want = port.analyze(x, y, 0.05, idx, n_steps=50, arctan=True)
+    got64 = capi.analyze_host(x, y, 0.05, idx, n_steps=50, precision=capi.FP64, arctan=True)
+    got32 = capi.analyze_host(x, y, 0.05, idx, n_steps=50, precision=capi.FP32, arctan=True)
+    assert rel_l2(got64, want) <= FP64_TOL
+    assert rel_l2(got32, want) <= FP32_TOL
+    lin = capi.analyze_host(x, y, 0.05, idx, n_steps=50, precision=capi.FP64)
+    assert rel_l2(lin, want) > 1e-3  # the operator matters
+
+
+def test_arctan_python_binding(capi, port):
+    import paper_2407_12168_b200 as tb
+    x, y, _, truth = conditioned_inputs(20, 2048)
+    y = np.arctan(truth) + 0.05
+    g = tb.GridSpec()
+    g.nx, g.ny = 32, 32
+    got = tb.ensf_analyze(x, g, y, r=0.1, n_steps=40, precision="fp64", obs_operator="arctan")
+    want = port.analyze(x, y, 0.1, None, n_steps=40, arctan=True)
+    assert rel_l2(got, want) <= FP64_TOL
