@@ -99,7 +99,18 @@ typedef struct turbda_ensf_params {
     int32_t device_count; /* >1 (host buffers only): split the window over       */
                           /* devices device .. device + device_count - 1         */
     uint32_t flags;       /* TURBDA_INPUTS_ON_DEVICE | TURBDA_ASYNC              */
+    int32_t score_mode;   /* TURBDA_SCORE_COMPONENTWISE (the reference) or        */
+                          /* TURBDA_SCORE_JOINT (north-star extension, fp64)      */
+    int32_t reserved;
 } turbda_ensf_params;
+
+/* score_mode */
+#define TURBDA_SCORE_COMPONENTWISE 0 /* proj/src/ensf.cpp:27-64: a softmax per coordinate */
+#define TURBDA_SCORE_JOINT 1         /* paper Eq. 15-16: one softmax per particle over   */
+                                     /* full-state distances; per pseudo-step one Gram   */
+                                     /* pass and, with a communicator, ONE allreduce of  */
+                                     /* the N x N (+2N) partial distances. fp64, no      */
+                                     /* minibatches. Parity unpinned (no reference).     */
 
 /* Fills *p with the reference defaults (include/turbda/ensf.hpp:22-27):
  * n_steps 100, eps 0.01, minibatch 0, damping_t 1, relax 1, fp32, device -1. */
@@ -151,6 +162,19 @@ int turbda_score(const double* z, int64_t d, double t, const double* forecast, i
 int turbda_diag(const double* members, int32_t n_members, int64_t d, const double* truth,
                 double* out, int32_t device, uint32_t flags, void* stream,
                 turbda_status* status);
+
+/*
+ * NCCL communicator for state-dimension sharding across processes (one rank
+ * per GPU).  Only the joint score mode exchanges data; the componentwise
+ * mode never needs it.  NCCL is loaded on first use (dlopen("libnccl.so.2"),
+ * the copy torch already loaded when present).
+ *   rank 0: turbda_comm_unique_id(id) -> broadcast the 128 bytes -> every
+ *   rank: turbda_comm_init(device, rank, world, id).
+ */
+int turbda_comm_unique_id(void* id128, turbda_status* status);
+int turbda_comm_init(int32_t device, int32_t rank, int32_t world, const void* id128,
+                     turbda_status* status);
+int turbda_comm_destroy(int32_t device);
 
 /* Number of CUDA devices (0 when none), library ABI version, and the name of
  * the kernel family compiled in ("sm_100a"). */

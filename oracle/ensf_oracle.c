@@ -32,6 +32,14 @@
  * reads sc[k] += damp * ((y - atan(z_k)) / r) / (1 + z_k^2) - the gradient
  * H'(z)^T R^-1 (y - h(z)); everything else is unchanged.
  *
+ * Extension (parity UNPINNED; paper Eq. 15-16, the estimator the reference
+ * rejects at proj/src/ensf.cpp:27-32): joint = 1 replaces the componentwise
+ * weights of mixture_score by one softmax per particle over the full-state
+ * squared distances, w_j = softmax_j(-sum_k (z_k - alpha x_jk)^2 / (2 beta^2))
+ * (row-minimum shift, fast_exp_nonpos), used for every coordinate.  On a
+ * window the distances must span the whole state, so joint runs take the
+ * whole state only (k0 = 0, dl = d_total).
+ *
  * Status codes follow include/turbda_b200.h: 0 ok, 1 config, 2 dimension,
  * 3 sampler diverged.
  */
@@ -154,6 +162,7 @@ typedef struct {
     double eps, damping_t;
     uint64_t seed, cycle;
     int j_batch;
+    int joint;            /* 1: joint-norm weights (extension) */
     const int* batches;   /* [n_steps][j_batch] or NULL for full batch */
     double* z;            /* [m][dl] particles */
     int* bad_step;        /* [m], -1 = finite throughout */
@@ -193,6 +202,35 @@ static void run_particle(orc_job* jb, int i) {
         const double inv2b = 1.0 / (2.0 * beta2);
         const int* batch = jb->batches ? jb->batches + (size_t)s * (size_t)jb->j_batch : full;
 
+        if (jb->joint) {
+            /* one weight per member from the full-state distance */
+            double dmin = INFINITY;
+            double* dist = num; /* scratch: j_batch <= dl is not guaranteed, use a heap array */
+            double* dj = malloc(sizeof(double) * (size_t)jb->j_batch);
+            for (int jj = 0; jj < jb->j_batch; ++jj) {
+                const double* xm = jb->x + (size_t)batch[jj] * (size_t)dl;
+                double acc = 0.0;
+                for (int64_t k = 0; k < dl; ++k) {
+                    const double diff = z[k] - alpha * xm[k];
+                    acc += diff * diff;
+                }
+                dj[jj] = acc;
+                dmin = acc < dmin ? acc : dmin;
+            }
+            (void)dist;
+            double dsum = 0.0;
+            for (int jj = 0; jj < jb->j_batch; ++jj) {
+                dj[jj] = orc_fast_exp_nonpos((dmin - dj[jj]) * inv2b);
+                dsum += dj[jj];
+            }
+            for (int64_t k = 0; k < dl; ++k) num[k] = 0.0;
+            for (int jj = 0; jj < jb->j_batch; ++jj) {
+                const double* xm = jb->x + (size_t)batch[jj] * (size_t)dl;
+                for (int64_t k = 0; k < dl; ++k) num[k] += dj[jj] * xm[k];
+            }
+            for (int64_t k = 0; k < dl; ++k) sc[k] = -(z[k] - alpha * num[k] / dsum) / beta2;
+            free(dj);
+        } else {
         for (int64_t k = 0; k < dl; ++k) mind2[k] = INFINITY;
         for (int jj = 0; jj < jb->j_batch; ++jj) {
             const double* xm = jb->x + (size_t)batch[jj] * (size_t)dl;
@@ -213,6 +251,7 @@ static void run_particle(orc_job* jb, int i) {
             }
         }
         for (int64_t k = 0; k < dl; ++k) sc[k] = -(z[k] - alpha * num[k] / den[k]) / beta2;
+        }
 
         if (jb->obs_kind == 0) {
             for (int64_t k = 0; k < dl; ++k) sc[k] += damp * ((jb->y[k] - z[k]) / jb->r[k]);
@@ -305,11 +344,13 @@ int orc_analyze(const double* x, int m, int64_t dl, int64_t k0, int64_t d_total,
                 const double* y, const double* r, const int64_t* idx, int64_t obs_dim,
                 int obs_kind, int n_steps, double eps, int minibatch_j, double damping_t,
                 double relax_factor, uint64_t seed, uint64_t cycle, int workers,
-                double* out, double* diverged_t) {
+                double* out, double* diverged_t, int joint) {
     if (!(eps > 0.0 && eps < 1.0) || n_steps < 10 || minibatch_j < 0 ||
         relax_factor < 0.0 || relax_factor > 1.0)
         return 1;
     if (m < 1 || dl < 0 || k0 < 0 || k0 + dl > d_total) return 2;
+    if (joint && (k0 != 0 || dl != d_total)) return 2;
+    if (joint && minibatch_j != 0 && minibatch_j < m) return 1;
     for (int64_t q = 0; q < obs_dim; ++q) if (!(r[q] > 0.0)) return 1;
     if (obs_kind < 0 || obs_kind > 3) return 1;
     if ((obs_kind == 0 || obs_kind == 2) && obs_dim != dl) return 2;
@@ -322,7 +363,7 @@ int orc_analyze(const double* x, int m, int64_t dl, int64_t k0, int64_t d_total,
     jb.x = x; jb.m = m; jb.dl = dl; jb.k0 = k0; jb.d_total = d_total;
     jb.y = y; jb.r = r; jb.idx = idx; jb.obs_dim = obs_dim; jb.obs_kind = obs_kind;
     jb.n_steps = n_steps; jb.eps = eps; jb.damping_t = damping_t;
-    jb.seed = seed; jb.cycle = cycle;
+    jb.seed = seed; jb.cycle = cycle; jb.joint = joint;
     jb.j_batch = (minibatch_j == 0 || minibatch_j >= m) ? m : minibatch_j;
     int* table = NULL;
     if (jb.j_batch != m) {

@@ -225,7 +225,7 @@ class PortOracle:
         L.orc_analyze.argtypes = [_dp, C.c_int, C.c_int64, C.c_int64, C.c_int64, _dp, _dp, _ip64,
                                   C.c_int64, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double,
                                   C.c_double, C.c_uint64, C.c_uint64, C.c_int, _dp,
-                                  C.POINTER(C.c_double)]
+                                  C.POINTER(C.c_double), C.c_int]
         L.orc_philox4x32.restype = None
         L.orc_philox4x32.argtypes = [_up32, _up32, _up32]
         L.orc_splitmix64.restype = C.c_uint64
@@ -248,9 +248,10 @@ class PortOracle:
 
     def analyze(self, members, y, r=1.0, idx=None, *, n_steps=100, eps=0.01, minibatch_j=0,
                 damping_t=1.0, relax_factor=1.0, seed=7, cycle=1, workers=0, k0=0,
-                d_total=None, arctan=False):
+                d_total=None, arctan=False, joint=False):
         """``members`` is the [m][dl] window starting at global coordinate k0.
-        ``arctan=True``: h(x) = atan(x) (extension, parity unpinned)."""
+        ``arctan=True``: h(x) = atan(x); ``joint=True``: joint-norm weights
+        (both extensions, parity unpinned)."""
         x = np.ascontiguousarray(members, dtype=np.float64)
         m, dl = x.shape
         d_total = dl if d_total is None else d_total
@@ -260,7 +261,7 @@ class PortOracle:
         workers = workers if workers > 0 else host_cores()
         code = self.lib.orc_analyze(x, m, dl, k0, d_total, y, r, idx_a, y.size, kind, n_steps,
                                     eps, minibatch_j, damping_t, relax_factor, seed, cycle,
-                                    workers, out, C.byref(div_t))
+                                    workers, out, C.byref(div_t), 1 if joint else 0)
         if code:
             raise OracleError(code, "", div_t.value)
         return out

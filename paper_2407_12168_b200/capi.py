@@ -17,6 +17,7 @@ import numpy as np
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libturbda_b200.so"
 
 OK, CONFIG, DIMENSION, DIVERGED, DOMAIN, CUDA, INTERNAL = range(7)
+SCORE_COMPONENTWISE, SCORE_JOINT = 0, 1
 FP32, FP64 = 0, 1
 INPUTS_ON_DEVICE = 0x1
 ASYNC = 0x2
@@ -29,7 +30,8 @@ class EnsfParams(C.Structure):
         ("minibatch_j", C.c_int32), ("obs_kind", C.c_int32), ("eps", C.c_double),
         ("damping_t", C.c_double), ("relax_factor", C.c_double), ("seed", C.c_uint64),
         ("cycle", C.c_uint64), ("precision", C.c_int32), ("device", C.c_int32),
-        ("device_count", C.c_int32), ("flags", C.c_uint32),
+        ("device_count", C.c_int32), ("flags", C.c_uint32), ("score_mode", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 
@@ -87,6 +89,12 @@ def lib() -> C.CDLL:
         L.turbda_profile_enable.restype = None
         L.turbda_profile_read.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
         L.turbda_profile_read.restype = C.c_int
+        L.turbda_comm_unique_id.argtypes = [C.c_void_p, C.POINTER(Status)]
+        L.turbda_comm_unique_id.restype = C.c_int
+        L.turbda_comm_init.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.POINTER(Status)]
+        L.turbda_comm_init.restype = C.c_int
+        L.turbda_comm_destroy.argtypes = [C.c_int32]
+        L.turbda_comm_destroy.restype = C.c_int
         _lib = L
     return _lib
 
@@ -138,7 +146,7 @@ def check(device: int, p: EnsfParams) -> Status:
 
 def analyze_host(members, y, r=1.0, idx=None, *, n_steps=100, eps=0.01, minibatch_j=0,
                  damping_t=1.0, relax_factor=1.0, seed=7, cycle=1, precision=FP32, device=-1,
-                 device_count=1, k0=0, d_total=None, arctan=False):
+                 device_count=1, k0=0, d_total=None, arctan=False, joint=False):
     """numpy-in / numpy-out analysis over the window [k0, k0 + d) of a state
     of dimension d_total (defaults to the whole state)."""
     x = np.ascontiguousarray(members, dtype=np.float64)
@@ -151,7 +159,8 @@ def analyze_host(members, y, r=1.0, idx=None, *, n_steps=100, eps=0.01, minibatc
                obs_kind=(0 if idx is None else 1) + (2 if arctan else 0), eps=eps,
                damping_t=damping_t,
                relax_factor=relax_factor, seed=seed, cycle=cycle, precision=precision,
-               device=device, device_count=device_count)
+               device=device, device_count=device_count,
+               score_mode=SCORE_JOINT if joint else SCORE_COMPONENTWISE)
     out = np.empty_like(x)
     analyze(p, x, y, r, ix, out)
     return out
@@ -198,6 +207,25 @@ def diag(members, truth=None, device=-1):
     _check(lib().turbda_diag(_ptr(x), x.shape[0], x.shape[1], _ptr(t), out, device, 0, None,
                              C.byref(st)), st)
     return float(out[0]), float(out[1])
+
+
+def comm_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    st = Status()
+    _check(lib().turbda_comm_unique_id(buf, C.byref(st)), st)
+    return bytes(buf)
+
+
+def comm_init(device: int, rank: int, world: int, uid: bytes) -> None:
+    """Library NCCL communicator for a state sharded over `world` processes
+    (used by the joint score mode's per-step allreduce)."""
+    buf = (C.c_char * 128).from_buffer_copy(uid)
+    st = Status()
+    _check(lib().turbda_comm_init(device, rank, world, buf, C.byref(st)), st)
+
+
+def comm_destroy(device: int) -> None:
+    lib().turbda_comm_destroy(device)
 
 
 def device_count() -> int:

@@ -16,6 +16,8 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include "ensf_device.h"
 #include "host_rng.h"
@@ -81,6 +83,9 @@ struct Workspace {
     cudaStream_t stream = nullptr;
     DevBuf x, z, xt, ab, steps, batches, status, out, y, r, idx;
     unsigned long long* status_host = nullptr;  // pinned
+    void* comm = nullptr;                       // ncclComm_t (joint mode, sharded)
+    int comm_world = 1;
+    DevBuf jpart, jred, jw;                     // joint-mode scratch
     std::vector<cudaStream_t> cstreams;         // host-mode chunk pipeline
     std::vector<cudaEvent_t> ev_chunk;
     cudaEvent_t ev_ready = nullptr;
@@ -187,6 +192,11 @@ int validate(const turbda_ensf_params* p, turbda_status* st) {
     if (p->precision != TURBDA_FP32 && p->precision != TURBDA_FP64)
         return fail(st, TURBDA_CONFIG, "ensf: precision must be fp32 (0) or fp64 (1)");
     if (p->n_members > (1 << 24)) return fail(st, TURBDA_CONFIG, "ensf: too many members");
+    if (p->score_mode != TURBDA_SCORE_COMPONENTWISE && p->score_mode != TURBDA_SCORE_JOINT)
+        return fail(st, TURBDA_CONFIG, "ensf: unknown score_mode");
+    if (p->score_mode == TURBDA_SCORE_JOINT && p->minibatch_j != 0 &&
+        p->minibatch_j < p->n_members)
+        return fail(st, TURBDA_CONFIG, "ensf: the joint score mode uses every member");
     return TURBDA_OK;
 }
 
@@ -505,6 +515,196 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
     return diverged(p, *w->status_host, st);
 }
 
+// --- NCCL, loaded on first use --------------------------------------------
+struct NcclApi {
+    bool tried = false, ok = false;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*comm_init_all)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                               ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+std::mutex g_nccl_mu;
+NcclApi g_nccl;
+
+NcclApi* nccl_api() {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (!g_nccl.tried) {
+        g_nccl.tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            g_nccl.get_unique_id = reinterpret_cast<decltype(g_nccl.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+            g_nccl.comm_init_rank = reinterpret_cast<decltype(g_nccl.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+            g_nccl.comm_init_all = reinterpret_cast<decltype(g_nccl.comm_init_all)>(dlsym(h, "ncclCommInitAll"));
+            g_nccl.all_reduce = reinterpret_cast<decltype(g_nccl.all_reduce)>(dlsym(h, "ncclAllReduce"));
+            g_nccl.comm_destroy = reinterpret_cast<decltype(g_nccl.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+            g_nccl.error_string = reinterpret_cast<decltype(g_nccl.error_string)>(dlsym(h, "ncclGetErrorString"));
+            g_nccl.ok = g_nccl.get_unique_id && g_nccl.comm_init_rank && g_nccl.comm_init_all &&
+                        g_nccl.all_reduce && g_nccl.comm_destroy && g_nccl.error_string;
+        }
+    }
+    return g_nccl.ok ? &g_nccl : nullptr;
+}
+
+int nccl_fail(turbda_status* st, NcclApi* api, ncclResult_t r, const char* where) {
+    return fail(st, TURBDA_CUDA, std::string(where) + ": " + (api ? api->error_string(r) : "nccl"));
+}
+
+// In-process cliques for device_count > 1 joint runs: comms[g] for device dev0 + g.
+std::mutex g_clique_mu;
+std::vector<std::pair<std::pair<int, int>, std::vector<ncclComm_t>>> g_cliques;
+
+int clique(int dev0, int ndev, std::vector<ncclComm_t>* out, turbda_status* st) {
+    std::lock_guard<std::mutex> lk(g_clique_mu);
+    for (auto& c : g_cliques)
+        if (c.first == std::make_pair(dev0, ndev)) {
+            *out = c.second;
+            return TURBDA_OK;
+        }
+    NcclApi* api = nccl_api();
+    if (!api) return fail(st, TURBDA_CUDA, "libnccl.so.2 not loadable");
+    std::vector<ncclComm_t> comms(static_cast<size_t>(ndev));
+    std::vector<int> devs(static_cast<size_t>(ndev));
+    for (int g = 0; g < ndev; ++g) devs[size_t(g)] = dev0 + g;
+    ncclResult_t r = api->comm_init_all(comms.data(), ndev, devs.data());
+    if (r != ncclSuccess) return nccl_fail(st, api, r, "ncclCommInitAll");
+    g_cliques.push_back({{dev0, ndev}, comms});
+    *out = comms;
+    return TURBDA_OK;
+}
+
+// Joint-norm analysis of one window on one device (joint_kernels.cu).  Host
+// mode copies X / obs in and the analysis out; `comm` (nullable) sums the
+// per-step [G | nz | nx] buffer over the ranks that share the state.
+int run_joint(const turbda_ensf_params* p, const Window& win, int device, const double* forecast,
+              const double* const* frows, const double* y, const double* r, const int64_t* idx,
+              double* out, double* const* orows, cudaStream_t user_stream, void* comm,
+              turbda_status* st) {
+    const bool on_dev = (p->flags & TURBDA_INPUTS_ON_DEVICE) != 0;
+    TB_CUDA(cudaSetDevice(device));
+    Workspace* w = workspace(device);
+    std::lock_guard<std::mutex> lk(w->mu);
+    if (int rc = ws_init(w, st)) return rc;
+    cudaStream_t s = user_stream ? user_stream : (on_dev ? cudaStreamLegacy : w->stream);
+    const int m = p->n_members;
+    const int64_t dl = win.dl;
+    const size_t md = size_t(m) * size_t(std::max<int64_t>(dl, 1));
+
+    const double *dx = forecast, *dy = y, *dr = r;
+    const int64_t* didx = idx;
+    double* dout = out;
+    const bool dense = obs_dense(p->obs_kind);
+    if (!on_dev) {
+        TB_CUDA(w->x.reserve(sizeof(double) * md));
+        TB_CUDA(w->out.reserve(sizeof(double) * md));
+        const size_t nb = size_t(std::max<int64_t>(dense ? dl : p->obs_dim, 1));
+        TB_CUDA(w->y.reserve(sizeof(double) * nb));
+        TB_CUDA(w->r.reserve(sizeof(double) * nb));
+        TB_CUDA(w->idx.reserve(sizeof(int64_t) * nb));
+        if (dl > 0) {
+            if (frows) {
+                for (int j = 0; j < m; ++j)
+                    TB_CUDA(cudaMemcpyAsync(w->x.as<double>() + size_t(j) * size_t(dl),
+                                            frows[j] + win.k0_local, sizeof(double) * size_t(dl),
+                                            cudaMemcpyHostToDevice, s));
+            } else {
+                TB_CUDA(cudaMemcpy2DAsync(w->x.p, sizeof(double) * size_t(dl),
+                                          forecast + win.k0_local, sizeof(double) * size_t(p->d_local),
+                                          sizeof(double) * size_t(dl), size_t(m),
+                                          cudaMemcpyHostToDevice, s));
+            }
+        }
+        const int64_t nobs = dense ? dl : p->obs_dim;
+        if (nobs > 0) {
+            TB_CUDA(cudaMemcpyAsync(w->y.p, dense ? y + win.k0_local : y, sizeof(double) * size_t(nobs),
+                                    cudaMemcpyHostToDevice, s));
+            TB_CUDA(cudaMemcpyAsync(w->r.p, dense ? r + win.k0_local : r, sizeof(double) * size_t(nobs),
+                                    cudaMemcpyHostToDevice, s));
+            if (!dense)
+                TB_CUDA(cudaMemcpyAsync(w->idx.p, idx, sizeof(int64_t) * size_t(nobs),
+                                        cudaMemcpyHostToDevice, s));
+        }
+        dx = w->x.as<double>();
+        dy = w->y.as<double>();
+        dr = w->r.as<double>();
+        didx = w->idx.as<int64_t>();
+        dout = w->out.as<double>();
+    }
+    const JointPlan pl = joint_plan(m, m, std::max<int64_t>(dl, 1));
+    TB_CUDA(w->z.reserve(sizeof(double) * md));
+    TB_CUDA(w->ab.reserve(sizeof(double2) * size_t(std::max<int64_t>(dl, 1))));
+    TB_CUDA(w->jpart.reserve(sizeof(double) * size_t(pl.nchunk) * pl.red_len));
+    TB_CUDA(w->jred.reserve(sizeof(double) * pl.red_len));
+    TB_CUDA(w->jw.reserve(sizeof(double) * size_t(m) * size_t(m)));
+    TB_CUDA(w->status.reserve(64));
+    unsigned long long* dstatus = w->status.as<unsigned long long>();
+    TB_CUDA(cudaMemsetAsync(dstatus, 0xff, sizeof(unsigned long long), s));
+
+    const int64_t k0g = p->k0 + win.k0_local;
+    TB_CUDA(launch_obs_prep(dense ? dy : dy, dr, didx, dense ? dl : p->obs_dim, p->obs_kind, k0g,
+                            dl, w->ab.as<double2>(), s));
+    KernelArgs a{};
+    a.d_total = p->d_total;
+    a.k0 = k0g;
+    a.dl = dl;
+    a.m = m;
+    a.n_steps = p->n_steps;
+    a.j_batch = m;
+    const uint64_t key = stream_key(p->seed, kUseEnsfParticles);
+    a.key0 = uint32_t(key);
+    a.key1 = uint32_t(key >> 32);
+    a.cycle_lo = uint32_t(p->cycle);
+    a.obs_atan = obs_arctan(p->obs_kind) ? 1 : 0;
+    double* z = w->z.as<double>();
+    TB_CUDA(launch_joint_init(a, z, s));
+    ProfPair prof;
+    if (g_profile.load() && on_dev) {
+        prof.device = device;
+        TB_CUDA(cudaEventCreate(&prof.a));
+        TB_CUDA(cudaEventCreate(&prof.b));
+        TB_CUDA(cudaEventRecord(prof.a, s));
+    }
+    const std::vector<StepTimes> grid = step_grid(p->n_steps, p->eps, p->damping_t);
+    NcclApi* api = comm ? nccl_api() : nullptr;
+    for (int step = 0; step < p->n_steps; ++step) {
+        const StepTimes& q = grid[size_t(step)];
+        const StepF64 c{q.alpha, q.beta2, 1.0 / (2.0 * q.beta2), q.b, q.s2, q.damp, q.sig, q.dt};
+        TB_CUDA(launch_joint_gram(a, pl, z, dx, w->jpart.as<double>(), w->jred.as<double>(), s));
+        if (comm) {
+            ncclResult_t rr = api->all_reduce(w->jred.p, w->jred.p, pl.red_len, ncclDouble, ncclSum,
+                                              static_cast<ncclComm_t>(comm), s);
+            if (rr != ncclSuccess) return nccl_fail(st, api, rr, "ncclAllReduce");
+        }
+        TB_CUDA(launch_joint_update(a, dx, w->ab.as<double2>(), w->jred.as<double>(), w->jw.as<double>(),
+                                    c, step, z, dstatus, s));
+    }
+    if (prof.a) {
+        TB_CUDA(cudaEventRecord(prof.b, s));
+        std::lock_guard<std::mutex> lk2(g_prof_mu);
+        g_prof_pending.push_back(prof);
+    }
+    TB_CUDA(launch_relax_f64(z, dx, m, dl, p->relax_factor, dout, s));
+    g_launches += 3 + 4 * uint64_t(p->n_steps);
+    if (on_dev && (p->flags & TURBDA_ASYNC)) return TURBDA_OK;
+    TB_CUDA(cudaMemcpyAsync(w->status_host, dstatus, sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s));
+    if (!on_dev && dl > 0) {
+        if (orows) {
+            for (int j = 0; j < m; ++j)
+                TB_CUDA(cudaMemcpyAsync(orows[j] + win.k0_local, dout + size_t(j) * size_t(dl),
+                                        sizeof(double) * size_t(dl), cudaMemcpyDeviceToHost, s));
+        } else {
+            TB_CUDA(cudaMemcpy2DAsync(out + win.k0_local, sizeof(double) * size_t(p->d_local), dout,
+                                      sizeof(double) * size_t(dl), sizeof(double) * size_t(dl),
+                                      size_t(m), cudaMemcpyDeviceToHost, s));
+        }
+    }
+    TB_CUDA(cudaStreamSynchronize(s));
+    return diverged(p, *w->status_host, st);
+}
+
 int resolve_device(int requested, turbda_status* st, int* out) {
     int n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);
@@ -566,9 +766,25 @@ int analyze_impl(const turbda_ensf_params* p, const double* forecast, const doub
         return fail(st, TURBDA_CONFIG, "device_count > 1 needs host buffers");
     if (p->d_local == 0) return TURBDA_OK;
 
-    if (ndev == 1)
+    const bool joint = p->score_mode == TURBDA_SCORE_JOINT;
+    if (ndev == 1) {
+        if (joint) {
+            // a window of a larger state shares the distances through the
+            // device's communicator (turbda_comm_init)
+            Workspace* w = workspace(dev0);
+            void* comm = (p->d_local < p->d_total && w->comm_world > 1) ? w->comm : nullptr;
+            if (p->d_local < p->d_total && !comm)
+                return fail(st, TURBDA_CONFIG,
+                            "joint score mode on a window needs turbda_comm_init on this device");
+            return run_joint(p, Window{0, p->d_local}, dev0, forecast, frows, y, r_diag, obs_idx,
+                             analysis_out, orows, static_cast<cudaStream_t>(stream), comm, st);
+        }
         return run_slice(p, Window{0, p->d_local}, dev0, forecast, frows, y, r_diag, obs_idx,
                          analysis_out, orows, static_cast<cudaStream_t>(stream), st);
+    }
+    std::vector<ncclComm_t> comms;
+    if (joint)
+        if (int rc = clique(dev0, ndev, &comms, st)) return rc;
 
     // state-dimension sharding: contiguous slices aligned to the 64-coordinate tile
     std::vector<Window> wins;
@@ -586,8 +802,11 @@ int analyze_impl(const turbda_ensf_params* p, const double* forecast, const doub
     for (int g = 0; g < ndev; ++g) {
         clear(&sts[size_t(g)]);
         th.emplace_back([&, g] {
-            rcs[size_t(g)] = run_slice(p, wins[size_t(g)], dev0 + g, forecast, frows, y, r_diag,
-                                       obs_idx, analysis_out, orows, nullptr, &sts[size_t(g)]);
+            rcs[size_t(g)] =
+                joint ? run_joint(p, wins[size_t(g)], dev0 + g, forecast, frows, y, r_diag, obs_idx,
+                                  analysis_out, orows, nullptr, comms[size_t(g)], &sts[size_t(g)])
+                      : run_slice(p, wins[size_t(g)], dev0 + g, forecast, frows, y, r_diag,
+                                  obs_idx, analysis_out, orows, nullptr, &sts[size_t(g)]);
         });
     }
     for (auto& t : th) t.join();
@@ -787,6 +1006,53 @@ int turbda_diag(const double* members, int32_t m, int64_t d, const double* truth
     ++g_launches;
     TB_CUDA(cudaMemcpyAsync(out, dsum, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     TB_CUDA(cudaStreamSynchronize(s));
+    return TURBDA_OK;
+}
+
+int turbda_comm_unique_id(void* id128, turbda_status* st) {
+    clear(st);
+    NcclApi* api = nccl_api();
+    if (!api) return fail(st, TURBDA_CUDA, "libnccl.so.2 not loadable");
+    ncclUniqueId id;
+    ncclResult_t r = api->get_unique_id(&id);
+    if (r != ncclSuccess) return nccl_fail(st, api, r, "ncclGetUniqueId");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id128, &id, sizeof id);
+    return TURBDA_OK;
+}
+
+int turbda_comm_init(int32_t device, int32_t rank, int32_t world, const void* id128,
+                     turbda_status* st) {
+    clear(st);
+    int dev = 0;
+    if (int rc = resolve_device(device, st, &dev)) return rc;
+    NcclApi* api = nccl_api();
+    if (!api) return fail(st, TURBDA_CUDA, "libnccl.so.2 not loadable");
+    TB_CUDA(cudaSetDevice(dev));
+    Workspace* w = workspace(dev);
+    std::lock_guard<std::mutex> lk(w->mu);
+    if (w->comm) {
+        api->comm_destroy(static_cast<ncclComm_t>(w->comm));
+        w->comm = nullptr;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof id);
+    ncclComm_t comm;
+    ncclResult_t r = api->comm_init_rank(&comm, world, id, rank);
+    if (r != ncclSuccess) return nccl_fail(st, api, r, "ncclCommInitRank");
+    w->comm = comm;
+    w->comm_world = world;
+    return TURBDA_OK;
+}
+
+int turbda_comm_destroy(int32_t device) {
+    if (device < 0 || cudaSetDevice(device) != cudaSuccess) return TURBDA_CUDA;
+    Workspace* w = workspace(device);
+    std::lock_guard<std::mutex> lk(w->mu);
+    NcclApi* api = nccl_api();
+    if (w->comm && api) api->comm_destroy(static_cast<ncclComm_t>(w->comm));
+    w->comm = nullptr;
+    w->comm_world = 1;
     return TURBDA_OK;
 }
 

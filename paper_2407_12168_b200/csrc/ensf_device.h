@@ -77,6 +77,24 @@ cudaError_t launch_score_f64(const double* z, const double* x, int m, int64_t d,
                              const double2* ab, double damp, int obs_atan, double* out,
                              cudaStream_t st);
 
+// --- joint-norm mode (north_star extension, joint_kernels.cu) ----------------
+struct JointPlan {
+    int nchunk = 1;       // coordinate chunks of the Gram pass
+    int64_t chunk = 16;   // coordinates per chunk
+    int tiles = 1;        // 64 x 64 output tiles
+    size_t red_len = 0;   // doubles in [G | nz | nx]
+};
+JointPlan joint_plan(int n, int m, int64_t dl);
+cudaError_t launch_joint_init(const KernelArgs& a, double* z, cudaStream_t st);
+// part: nchunk * red_len doubles of scratch; red: red_len doubles (the
+// buffer a multi-GPU run allreduces)
+cudaError_t launch_joint_gram(const KernelArgs& a, const JointPlan& pl, const double* z,
+                              const double* x, double* part, double* red, cudaStream_t st);
+// wn: m * m doubles of scratch
+cudaError_t launch_joint_update(const KernelArgs& a, const double* x, const double2* ab,
+                                const double* red, double* wn, const StepF64& c, int step,
+                                double* z, unsigned long long* status, cudaStream_t st);
+
 // rmse / spread partial sums: out[0] = sum (mean - truth)^2, out[1] = sum dev^2
 cudaError_t launch_diag(const double* x, int m, int64_t d, const double* truth, double* out,
                         cudaStream_t st);

@@ -43,7 +43,7 @@ py::array_t<double> ensf_analyze(const darray& members, const turbda::GridSpec& 
                                  int /*workers*/, int thinning, const std::string& precision,
                                  int device, int device_count, double eps, int minibatch_j,
                                  double damping_t, const std::string& obs_operator,
-                                 py::object out_obj) {
+                                 const std::string& score_mode, py::object out_obj) {
     if (members.ndim() != 2) throw turbda::DimensionError("members must be (M, d)");
     const auto m = members.shape(0);
     const auto d = members.shape(1);
@@ -71,6 +71,9 @@ py::array_t<double> ensf_analyze(const darray& members, const turbda::GridSpec& 
     if (obs_operator != "linear" && obs_operator != "arctan")
         throw turbda::ConfigError("obs_operator must be 'linear' or 'arctan'");
     p.obs_kind = (thinning > 1 ? 1 : 0) + (obs_operator == "arctan" ? 2 : 0);
+    if (score_mode != "componentwise" && score_mode != "joint")
+        throw turbda::ConfigError("score_mode must be 'componentwise' or 'joint'");
+    p.score_mode = score_mode == "joint" ? TURBDA_SCORE_JOINT : TURBDA_SCORE_COMPONENTWISE;
     p.eps = eps;
     p.damping_t = damping_t;
     p.relax_factor = relax_factor;
@@ -125,7 +128,8 @@ PYBIND11_MODULE(_core, mod) {
             py::kw_only(), py::arg("thinning") = 0, py::arg("precision") = "fp32",
             py::arg("device") = -1, py::arg("device_count") = 1, py::arg("eps") = 0.01,
             py::arg("minibatch_j") = 0, py::arg("damping_t") = 1.0,
-            py::arg("obs_operator") = "linear", py::arg("out") = py::none(),
+            py::arg("obs_operator") = "linear", py::arg("score_mode") = "componentwise",
+            py::arg("out") = py::none(),
             "EnSF analysis of an (M, d) float64 forecast ensemble on the GPU; returns (M, d)");
 
     mod.def("device_count", &turbda_device_count);

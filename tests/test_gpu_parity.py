@@ -241,3 +241,55 @@ def test_arctan_python_binding(capi, port):
     got = tb.ensf_analyze(x, g, y, r=0.1, n_steps=40, precision="fp64", obs_operator="arctan")
     want = port.analyze(x, y, 0.1, None, n_steps=40, arctan=True)
     assert rel_l2(got, want) <= FP64_TOL
+
+
+# --- extension: joint-norm score (north_star; paper Eq. 15-16) ---------------
+# The reference rejects this estimator (proj/src/ensf.cpp:27-32); the oracle is
+# the C restatement with the weight line changed, parity UNPINNED.  The GPU
+# forms the distances through the fp64 Gram identity, the oracle sums squared
+# differences directly: agreement to ~1e-12 relative in D, hence 1e-9 here.
+JOINT_TOL = 1e-9
+
+
+@pytest.mark.parametrize("m,d,stride", [(20, 1024, 1), (64, 3000, 4), (33, 257, 1)])
+def test_joint_mode_vs_port(capi, port, m, d, stride):
+    x, y, idx, _ = conditioned_inputs(m, d, stride=stride)
+    # weak obs and a wide prior keep the joint softmax away from one-hot
+    want = port.analyze(0.05 * x, y, 4.0, idx, n_steps=20, joint=True)
+    got = capi.analyze_host(0.05 * x, y, 4.0, idx, n_steps=20, joint=True)
+    assert rel_l2(got, want) <= JOINT_TOL, rel_l2(got, want)
+    comp = capi.analyze_host(0.05 * x, y, 4.0, idx, n_steps=20)
+    assert rel_l2(comp, want) > 1e-3  # a different estimator
+
+
+def test_joint_mode_arctan_and_binding(capi, port):
+    import paper_2407_12168_b200 as tb
+    x, y, _, truth = conditioned_inputs(16, 2048)
+    y = np.arctan(truth) + 0.05
+    g = tb.GridSpec()
+    g.nx, g.ny = 32, 32
+    got = tb.ensf_analyze(0.1 * x, g, y, r=0.5, n_steps=30, obs_operator="arctan",
+                          score_mode="joint")
+    want = port.analyze(0.1 * x, y, 0.5, None, n_steps=30, arctan=True, joint=True)
+    assert rel_l2(got, want) <= JOINT_TOL
+
+
+def test_joint_mode_multi_device(capi, port):
+    n = capi.device_count()
+    if n < 2:
+        pytest.skip("one device")
+    x, y, _, _ = conditioned_inputs(20, 5000)
+    want = port.analyze(0.05 * x, y, 4.0, None, n_steps=20, joint=True)
+    got = capi.analyze_host(0.05 * x, y, 4.0, None, n_steps=20, joint=True, device=0,
+                            device_count=n)
+    assert rel_l2(got, want) <= JOINT_TOL
+
+
+def test_joint_mode_rejects_minibatch_and_uncommunicated_window(capi):
+    x, y, _, _ = conditioned_inputs(8, 64)
+    with pytest.raises(capi.TurbdaError) as ei:
+        capi.analyze_host(x, y, n_steps=10, joint=True, minibatch_j=3)
+    assert ei.value.code == capi.CONFIG
+    with pytest.raises(capi.TurbdaError) as ei:
+        capi.analyze_host(x[:, :32], y[:32], n_steps=10, joint=True, k0=0, d_total=64)
+    assert ei.value.code == capi.CONFIG
