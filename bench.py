@@ -192,6 +192,9 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
+    ap.add_argument("--score", choices=["componentwise", "joint"], default="componentwise",
+                    help="joint: the north-star joint-norm extension (fp64, one NCCL allreduce "
+                         "of the N x N distances per pseudo-step across ranks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-d", type=int, default=32768)
     ap.add_argument("--ref-sample-d", type=int, default=8192)
@@ -221,7 +224,13 @@ def main():
     d, m, s, stride, desc = CONFIGS[args.config]
     d_total = d * world
     k0 = rank * d
+    joint = args.score == "joint"
+    # joint mode: distances/update in fp64 always; --precision picks the noise
     prec = capi.FP32 if args.precision == "fp32" else capi.FP64
+    if joint and world > 1:
+        uid = [capi.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        capi.comm_init(local, rank, world, uid[0])
 
     # --- resident inputs: 3 rotating sets so the working set exceeds L2 ----
     n_sets = 3
@@ -237,7 +246,8 @@ def main():
     obs_dim = host_sets[0][1].size
     p = capi.params(d_total=d_total, k0=k0, d_local=d, obs_dim=obs_dim, n_members=m, n_steps=s,
                     obs_kind=0 if stride <= 1 else 1, precision=prec, device=local,
-                    flags=capi.INPUTS_ON_DEVICE | capi.ASYNC)
+                    flags=capi.INPUTS_ON_DEVICE | capi.ASYNC,
+                    score_mode=capi.SCORE_JOINT if joint else capi.SCORE_COMPONENTWISE)
     stream = torch.cuda.Stream(dev)  # a real stream: the events and kernels share it
     torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
@@ -313,9 +323,18 @@ def main():
         dist.barrier()
     for q in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        res = tb.ensf_analyze(hx, grid, hy_full, r=1.0, seed=7, cycle=1 + q, n_steps=s,
-                              thinning=stride if stride > 1 else 0,
-                              precision=args.precision, device=local, out=hout)
+        if joint and world > 1:
+            # a window of the sharded state: the C-ABI with host buffers
+            pe = capi.params(d_total=d_total, k0=k0, d_local=d, obs_dim=obs_dim, n_members=m,
+                             n_steps=s, obs_kind=0 if stride <= 1 else 1, precision=prec,
+                             device=local, cycle=1 + q, score_mode=capi.SCORE_JOINT)
+            capi.analyze(pe, hx, hy_full, np.ones_like(hy_full), host_sets[0][2], hout)
+            res = hout
+        else:
+            res = tb.ensf_analyze(hx, grid, hy_full, r=1.0, seed=7, cycle=1 + q, n_steps=s,
+                                  thinning=stride if stride > 1 else 0,
+                                  precision=args.precision, device=local,
+                                  score_mode=args.score, out=hout)
         if q >= args.warmup:
             e2e_times.append(time.perf_counter() - t0)
     e2e_s = torch.tensor([sum(e2e_times) / len(e2e_times)], dtype=torch.float64, device=dev)
@@ -330,7 +349,10 @@ def main():
     # --- roofline of the fused analysis kernel -------------------------------
     pk, pk_kind = peaks()
     units_per_launch = units_per_gpu
-    achieved_gbs = BYTES_PER_UNIT * units_per_launch / (kern_ms / 1e3) / 1e9
+    # joint mode streams Z and X every pseudo-step in fp64: z read twice and
+    # written once (24 B) + two passes over X amortised over N particles
+    bytes_per_unit = (24 + 16 * m / m) if joint else BYTES_PER_UNIT
+    achieved_gbs = bytes_per_unit * units_per_launch / (kern_ms / 1e3) / 1e9
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
@@ -340,26 +362,33 @@ def main():
             traffic = None
     pair_evals = units_per_launch * m
     mufu_peak = MUFU_PER_CLK_PER_SM * 148 * pk.get("sm_max_mhz", 1965.0) * 1e6
+    fp64_peak = 64 * 2 * 148 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
     roofline = {
         "bound": "hbm", "achieved": achieved_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
         "frac": achieved_gbs / pk["hbm_gbs"], "traffic": traffic,
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})",
-        "algorithmic_bytes_per_unit": BYTES_PER_UNIT, "units_per_launch": units_per_launch,
-        "kernel": "ensf_f32_kernel" if prec == capi.FP32 else "ensf_f64_kernel",
+        "algorithmic_bytes_per_unit": bytes_per_unit, "units_per_launch": units_per_launch,
+        "kernel": ("joint: gram_partial + reduce + allreduce + softmax + apply, all steps" if joint
+                   else "ensf_f32_kernel" if prec == capi.FP32 else "ensf_f64_kernel"),
         "kernel_ms": kern_ms, "kernel_share_of_step": kern_ms / ms,
-        "binding_roofline": {
+        "binding_roofline": ({
             "bound": "sfu (MUFU.EX2, one exp per pair-eval)",
             "achieved": pair_evals / (kern_ms / 1e3), "unit": "pair-evals/s",
             "peak": mufu_peak, "frac": pair_evals / (kern_ms / 1e3) / mufu_peak,
-            "peak_source": "16 ex2/clk/SM measured x 148 SMs x sm_max_mhz"},
+            "peak_source": "16 ex2/clk/SM measured x 148 SMs x sm_max_mhz"} if not joint else {
+            "bound": "fp64 pipe (Gram + weighted sum: 2 DFMA per pair-eval)",
+            "achieved": 4.0 * pair_evals / (kern_ms / 1e3) / 1e12, "unit": "TFLOP/s",
+            "peak": fp64_peak, "frac": 4.0 * pair_evals / (kern_ms / 1e3) / 1e12 / fp64_peak,
+            "peak_source": "64 DFMA/clk/SM (tools/pipe_microbench: 59 measured) x 2 x 148 x sm_max_mhz"}),
     }
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32" if prec == capi.FP32 else "f64",
+        "vs_baseline": None, "dtype": "f64" if (joint or prec == capi.FP64) else "f32",
         "data": "synthetic",
-        "config": {"workload": desc, "d_per_gpu": d, "d_total": d_total, "members": m,
+        "config": {"workload": desc + (" [joint-norm score extension]" if joint else ""),
+                   "score": args.score, "d_per_gpu": d, "d_total": d_total, "members": m,
                    "pseudo_steps": s, "obs_stride": stride,
                    "l2": (f"L2 flushed (512 MB write) before each step, outside its timing; "
                           f"inputs {set_bytes / 1e6:.0f} MB" if flush else
@@ -381,6 +410,8 @@ def main():
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if joint and world > 1:
+        capi.comm_destroy(local)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -109,7 +109,9 @@ typedef struct turbda_ensf_params {
 #define TURBDA_SCORE_JOINT 1         /* paper Eq. 15-16: one softmax per particle over   */
                                      /* full-state distances; per pseudo-step one Gram   */
                                      /* pass and, with a communicator, ONE allreduce of  */
-                                     /* the N x N (+2N) partial distances. fp64, no      */
+                                     /* the N x N (+2N) partial distances. Distances and */
+                                     /* the update in fp64; TURBDA_FP32 only switches    */
+                                     /* the particle noise to the fp32 Box-Muller. No    */
                                      /* minibatches. Parity unpinned (no reference).     */
 
 /* Fills *p with the reference defaults (include/turbda/ensf.hpp:22-27):

@@ -678,7 +678,7 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
             if (rr != ncclSuccess) return nccl_fail(st, api, rr, "ncclAllReduce");
         }
         TB_CUDA(launch_joint_update(a, dx, w->ab.as<double2>(), w->jred.as<double>(), w->jw.as<double>(),
-                                    c, step, z, dstatus, s));
+                                    c, step, z, dstatus, p->precision == TURBDA_FP32, s));
     }
     if (prof.a) {
         TB_CUDA(cudaEventRecord(prof.b, s));

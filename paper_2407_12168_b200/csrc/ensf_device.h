@@ -91,9 +91,11 @@ cudaError_t launch_joint_init(const KernelArgs& a, double* z, cudaStream_t st);
 cudaError_t launch_joint_gram(const KernelArgs& a, const JointPlan& pl, const double* z,
                               const double* x, double* part, double* red, cudaStream_t st);
 // wn: m * m doubles of scratch
+// f32_noise: particle normals from the fp32 Box-Muller (TURBDA_FP32)
 cudaError_t launch_joint_update(const KernelArgs& a, const double* x, const double2* ab,
                                 const double* red, double* wn, const StepF64& c, int step,
-                                double* z, unsigned long long* status, cudaStream_t st);
+                                double* z, unsigned long long* status, bool f32_noise,
+                                cudaStream_t st);
 
 // rmse / spread partial sums: out[0] = sum (mean - truth)^2, out[1] = sum dev^2
 cudaError_t launch_diag(const double* x, int m, int64_t d, const double* truth, double* out,

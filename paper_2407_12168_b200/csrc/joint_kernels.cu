@@ -184,44 +184,86 @@ __global__ void joint_softmax_kernel(const double* __restrict__ red, int n, int 
 }
 
 // xbar_ik = sum_j w_ij x_jk; posterior score; Euler-Maruyama in place.
-// Thread = (coordinate pair, particle blockIdx.y).
-__global__ void joint_apply_kernel(KernelArgs a, const double* __restrict__ x,
-                                   const double2* __restrict__ ab, const double* __restrict__ wn,
-                                   StepF64 c, int step, double* __restrict__ z,
-                                   unsigned long long* __restrict__ status) {
-    const int64_t kl = 2 * (int64_t(blockIdx.x) * blockDim.x + threadIdx.x);
-    const int i = blockIdx.y;
-    if (kl >= a.dl) return;
-    const bool has_y = kl + 1 < a.dl;
-    const double* w = wn + size_t(i) * a.m;
-    double sx = 0.0, sy = 0.0;
-    for (int j = 0; j < a.m; ++j) {
-        const double wj = __ldg(w + j);
-        const double* xr = x + size_t(j) * size_t(a.dl) + kl;
-        sx = fma(wj, __ldg(xr), sx);
-        if (has_y) sy = fma(wj, __ldg(xr + 1), sy);
+// CTA = 64 coordinates (lane = coordinate pair) x kJW warps x kJP particles
+// per warp; member rows are staged through shared memory 64 at a time, so a
+// loaded x pair feeds kJP particles.  kF32Noise: the particle normals come
+// from the fp32 Box-Muller of the fast path (the update stays fp64).
+constexpr int kJP = 8, kJW = 4, kJM = 64;
+
+template <bool kF32Noise>
+__global__ void __launch_bounds__(kJW * 32) joint_apply_kernel(
+    KernelArgs a, const double* __restrict__ x, const double2* __restrict__ ab,
+    const double* __restrict__ wn, StepF64 c, int step, double* __restrict__ z,
+    unsigned long long* __restrict__ status) {
+    __shared__ double2 xs[kJM][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t kl = int64_t(blockIdx.x) * 64 + 2 * lane;
+    const int i0 = (blockIdx.y * kJW + warp) * kJP;
+    const bool has_x = kl < a.dl, has_y = kl + 1 < a.dl;
+    const bool aligned = (a.dl & 1) == 0;
+    double sx[kJP], sy[kJP];
+#pragma unroll
+    for (int p = 0; p < kJP; ++p) sx[p] = sy[p] = 0.0;
+    for (int j0 = 0; j0 < a.m; j0 += kJM) {
+        const int jn = a.m - j0 < kJM ? a.m - j0 : kJM;
+        __syncthreads();
+        for (int q = threadIdx.x; q < jn * 32; q += kJW * 32) {
+            const int jj = q >> 5, l = q & 31;
+            const int64_t k = int64_t(blockIdx.x) * 64 + 2 * l;
+            const double* row = x + size_t(j0 + jj) * size_t(a.dl);
+            double2 v = make_double2(0.0, 0.0);
+            if (k + 1 < a.dl)
+                v = aligned ? __ldg(reinterpret_cast<const double2*>(row + k))
+                            : make_double2(__ldg(row + k), __ldg(row + k + 1));
+            else if (k < a.dl)
+                v.x = __ldg(row + k);
+            xs[jj][l] = v;
+        }
+        __syncthreads();
+        for (int jj = 0; jj < jn; ++jj) {
+            const double2 xv = xs[jj][lane];
+#pragma unroll
+            for (int p = 0; p < kJP; ++p) {
+                const int i = i0 + p < a.m ? i0 + p : a.m - 1;
+                const double w = __ldg(wn + size_t(i) * a.m + j0 + jj);  // warp-uniform
+                sx[p] = fma(w, xv.x, sx[p]);
+                sy[p] = fma(w, xv.y, sy[p]);
+            }
+        }
     }
-    double* zr = z + size_t(i) * size_t(a.dl) + kl;
-    double zx = zr[0], zy = has_y ? zr[1] : 0.0;
+    if (!has_x) return;
     const double2 o0 = ab[kl];
     const double2 o1 = has_y ? ab[kl + 1] : make_double2(0.0, 0.0);
-    double scx = -(zx - c.alpha * sx) / c.beta2;
-    double scy = -(zy - c.alpha * sy) / c.beta2;
-    if (a.obs_atan) {
-        scx += c.damp * ((o0.y - o0.x * atan(zx)) / (1.0 + zx * zx));
-        scy += c.damp * ((o1.y - o1.x * atan(zy)) / (1.0 + zy * zy));
-    } else {
-        scx += c.damp * (o0.y - o0.x * zx);
-        scy += c.damp * (o1.y - o1.x * zy);
-    }
     const uint64_t n0 = uint64_t(step + 1) * uint64_t(a.d_total) + uint64_t(a.k0 + kl);
-    const double2 xi = normal_pair_f64(n0, uint32_t(i), a.cycle_lo, a.key0, a.key1);
-    zx += -(c.b * zx - c.s2 * scx) * c.dt + c.sig * xi.x;
-    zy += -(c.b * zy - c.s2 * scy) * c.dt + c.sig * xi.y;
-    zr[0] = zx;
-    if (has_y) zr[1] = zy;
-    if (!isfinite(zx) || (has_y && !isfinite(zy)))
-        atomicMin(status, (uint64_t(i) << 32) | uint32_t(step));
+#pragma unroll
+    for (int p = 0; p < kJP; ++p) {
+        const int i = i0 + p;
+        if (i >= a.m) break;
+        double* zr = z + size_t(i) * size_t(a.dl) + kl;
+        double zx = zr[0], zy = has_y ? zr[1] : 0.0;
+        double scx = -(zx - c.alpha * sx[p]) / c.beta2;
+        double scy = -(zy - c.alpha * sy[p]) / c.beta2;
+        if (a.obs_atan) {
+            scx += c.damp * ((o0.y - o0.x * atan(zx)) / (1.0 + zx * zx));
+            scy += c.damp * ((o1.y - o1.x * atan(zy)) / (1.0 + zy * zy));
+        } else {
+            scx += c.damp * (o0.y - o0.x * zx);
+            scy += c.damp * (o1.y - o1.x * zy);
+        }
+        double2 xi;
+        if (kF32Noise) {
+            const float2 f = normal_pair_f32(n0, uint32_t(i), a.cycle_lo, a.key0, a.key1);
+            xi = make_double2(f.x, f.y);
+        } else {
+            xi = normal_pair_f64(n0, uint32_t(i), a.cycle_lo, a.key0, a.key1);
+        }
+        zx += -(c.b * zx - c.s2 * scx) * c.dt + c.sig * xi.x;
+        zy += -(c.b * zy - c.s2 * scy) * c.dt + c.sig * xi.y;
+        zr[0] = zx;
+        if (has_y) zr[1] = zy;
+        if (!isfinite(zx) || (has_y && !isfinite(zy)))
+            atomicMin(status, (uint64_t(i) << 32) | uint32_t(step));
+    }
 }
 
 }  // namespace
@@ -264,13 +306,17 @@ cudaError_t launch_joint_gram(const KernelArgs& a, const JointPlan& pl, const do
 
 cudaError_t launch_joint_update(const KernelArgs& a, const double* x, const double2* ab,
                                 const double* red, double* wn, const StepF64& c, int step,
-                                double* z, unsigned long long* status, cudaStream_t st) {
+                                double* z, unsigned long long* status, bool f32_noise,
+                                cudaStream_t st) {
     joint_softmax_kernel<<<unsigned((a.m + 3) / 4), 128, 0, st>>>(red, a.m, a.m, c.alpha, c.inv2b,
                                                                   wn);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || a.dl <= 0) return e;
-    const dim3 grid(unsigned((a.dl / 2 + 127) / 128 + 1), unsigned(a.m));
-    joint_apply_kernel<<<grid, 128, 0, st>>>(a, x, ab, wn, c, step, z, status);
+    const dim3 grid(unsigned((a.dl + 63) / 64), unsigned((a.m + kJP * kJW - 1) / (kJP * kJW)));
+    if (f32_noise)
+        joint_apply_kernel<true><<<grid, kJW * 32, 0, st>>>(a, x, ab, wn, c, step, z, status);
+    else
+        joint_apply_kernel<false><<<grid, kJW * 32, 0, st>>>(a, x, ab, wn, c, step, z, status);
     return cudaGetLastError();
 }
 

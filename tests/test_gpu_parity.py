@@ -256,8 +256,10 @@ def test_joint_mode_vs_port(capi, port, m, d, stride):
     x, y, idx, _ = conditioned_inputs(m, d, stride=stride)
     # weak obs and a wide prior keep the joint softmax away from one-hot
     want = port.analyze(0.05 * x, y, 4.0, idx, n_steps=20, joint=True)
-    got = capi.analyze_host(0.05 * x, y, 4.0, idx, n_steps=20, joint=True)
+    got = capi.analyze_host(0.05 * x, y, 4.0, idx, n_steps=20, joint=True, precision=capi.FP64)
     assert rel_l2(got, want) <= JOINT_TOL, rel_l2(got, want)
+    got32 = capi.analyze_host(0.05 * x, y, 4.0, idx, n_steps=20, joint=True, precision=capi.FP32)
+    assert rel_l2(got32, want) <= FP32_TOL  # fp32 particle noise only
     comp = capi.analyze_host(0.05 * x, y, 4.0, idx, n_steps=20)
     assert rel_l2(comp, want) > 1e-3  # a different estimator
 
@@ -269,7 +271,7 @@ def test_joint_mode_arctan_and_binding(capi, port):
     g = tb.GridSpec()
     g.nx, g.ny = 32, 32
     got = tb.ensf_analyze(0.1 * x, g, y, r=0.5, n_steps=30, obs_operator="arctan",
-                          score_mode="joint")
+                          score_mode="joint", precision="fp64")
     want = port.analyze(0.1 * x, y, 0.5, None, n_steps=30, arctan=True, joint=True)
     assert rel_l2(got, want) <= JOINT_TOL
 
@@ -281,7 +283,7 @@ def test_joint_mode_multi_device(capi, port):
     x, y, _, _ = conditioned_inputs(20, 5000)
     want = port.analyze(0.05 * x, y, 4.0, None, n_steps=20, joint=True)
     got = capi.analyze_host(0.05 * x, y, 4.0, None, n_steps=20, joint=True, device=0,
-                            device_count=n)
+                            device_count=n, precision=capi.FP64)
     assert rel_l2(got, want) <= JOINT_TOL
 
 
@@ -293,3 +295,18 @@ def test_joint_mode_rejects_minibatch_and_uncommunicated_window(capi):
     with pytest.raises(capi.TurbdaError) as ei:
         capi.analyze_host(x[:, :32], y[:32], n_steps=10, joint=True, k0=0, d_total=64)
     assert ei.value.code == capi.CONFIG
+
+
+def test_joint_mode_multi_process_nccl(capi):
+    """torchrun over every visible GPU: per-step NCCL allreduce of the
+    distance partials through the library communicator."""
+    import subprocess
+    import sys
+    n = capi.device_count()
+    if n < 2:
+        pytest.skip("one device")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29533",
+           str(ROOT / "tools" / "joint_multiproc_check.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert "JOINT_MULTIPROC_OK" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]

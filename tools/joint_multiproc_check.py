@@ -1,0 +1,63 @@
+"""Multi-process joint-norm check (run under torchrun, one rank per GPU).
+
+Each rank analyses its contiguous shard of a d-coordinate state with the joint
+score; the library's NCCL communicator (turbda_comm_init) sums the per-step
+N x N (+2N) distance partials - the one collective of the path.  Rank 0
+gathers the shards and compares with the C oracle on the whole state, and
+checks the componentwise mode reassembles bit-exactly with no collective.
+
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/joint_multiproc_check.py
+"""
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+from oracle.oracle import PortOracle, conditioned_inputs, rel_l2  # noqa: E402
+from paper_2407_12168_b200 import capi  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    uid = [capi.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    capi.comm_init(local, rank, world, uid[0])
+
+    m, d = 20, 6000
+    x, y, _, _ = conditioned_inputs(m, d)
+    x = 0.05 * x
+    lo, hi = d * rank // world, d * (rank + 1) // world
+    part_j = capi.analyze_host(x[:, lo:hi], y[lo:hi], 4.0, None, n_steps=20, joint=True,
+                               device=local, k0=lo, d_total=d, precision=capi.FP64)
+    part_c = capi.analyze_host(x[:, lo:hi], y[lo:hi], 4.0, None, n_steps=20, device=local,
+                               k0=lo, d_total=d)
+    parts = [None] * world
+    dist.all_gather_object(parts, (lo, part_j, part_c))
+    if rank == 0:
+        parts.sort(key=lambda t: t[0])
+        got_j = np.concatenate([p[1] for p in parts], axis=1)
+        got_c = np.concatenate([p[2] for p in parts], axis=1)
+        port = PortOracle()
+        want_j = port.analyze(x, y, 4.0, None, n_steps=20, joint=True)
+        whole_c = capi.analyze_host(x, y, 4.0, None, n_steps=20, device=local)
+        ej = rel_l2(got_j, want_j)
+        print(f"joint sharded x{world} vs oracle rel-L2 {ej:.3e}; componentwise shards bitwise "
+              f"{np.array_equal(got_c, whole_c)}", flush=True)
+        ok = ej <= 1e-9 and np.array_equal(got_c, whole_c)
+        print("JOINT_MULTIPROC_OK" if ok else "JOINT_MULTIPROC_FAIL", flush=True)
+    capi.comm_destroy(local)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
