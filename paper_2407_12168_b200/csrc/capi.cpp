@@ -635,7 +635,7 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
     const JointPlan pl = joint_plan(m, m, std::max<int64_t>(dl, 1));
     TB_CUDA(w->z.reserve(sizeof(double) * md));
     TB_CUDA(w->ab.reserve(sizeof(double2) * size_t(std::max<int64_t>(dl, 1))));
-    TB_CUDA(w->jpart.reserve(sizeof(double) * size_t(pl.nchunk) * pl.red_len));
+    TB_CUDA(w->jpart.reserve(sizeof(double) * pl.scratch));
     TB_CUDA(w->jred.reserve(sizeof(double) * pl.red_len));
     TB_CUDA(w->jw.reserve(sizeof(double) * size_t(m) * size_t(m)));
     TB_CUDA(w->status.reserve(64));

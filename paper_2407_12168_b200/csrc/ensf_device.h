@@ -83,10 +83,11 @@ struct JointPlan {
     int64_t chunk = 16;   // coordinates per chunk
     int tiles = 1;        // 64 x 64 output tiles
     size_t red_len = 0;   // doubles in [G | nz | nx]
+    size_t scratch = 0;   // doubles of `part` scratch launch_joint_gram needs
 };
 JointPlan joint_plan(int n, int m, int64_t dl);
 cudaError_t launch_joint_init(const KernelArgs& a, double* z, cudaStream_t st);
-// part: nchunk * red_len doubles of scratch; red: red_len doubles (the
+// part: plan.scratch doubles; red: red_len doubles (the
 // buffer a multi-GPU run allreduces)
 cudaError_t launch_joint_gram(const KernelArgs& a, const JointPlan& pl, const double* z,
                               const double* x, double* part, double* red, cudaStream_t st);

@@ -73,83 +73,115 @@ __global__ void joint_init_kernel(KernelArgs a, double* __restrict__ z) {
     if (kl + 1 < a.dl) row[kl + 1] = v.y;
 }
 
-// Partial Gram over coordinate chunk blockIdx.x for output tile blockIdx.y.
-// 256 threads, 4 x 4 accumulators each; Z and X stages transposed in shared
-// memory with a one-double pad (conflict-free column reads).
+// Partial Gram over coordinate chunk blockIdx.x for output tile blockIdx.y on
+// the FP64 tensor cores: DMMA.8x8x4 (mma.sync m8n8k4 f64).  Warp w owns the
+// 8-row strip [8w, 8w+8) of the 64 x 64 tile (8 accumulator fragments).  Z
+// and X stages stay row-major in shared memory with a row stride of 20
+// doubles, which makes both fragment loads 2-wavefront (bank-conflict free
+// for 64-bit accesses).  The squared norms are summed from the staging loads.
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+constexpr int kStride = kK + 4;
+
 __global__ void __launch_bounds__(256) gram_partial_kernel(const double* __restrict__ z,
                                                            const double* __restrict__ x, int n,
                                                            int m, int64_t dl, int64_t chunk,
                                                            double* __restrict__ part) {
-    __shared__ double zs[kK][kT + 1];
-    __shared__ double xs[kK][kT + 1];
+    __shared__ double zs[kT][kStride];
+    __shared__ double xs[kT][kStride];
     const int ntj = (m + kT - 1) / kT;
     const int ti0 = (blockIdx.y / ntj) * kT, tj0 = (blockIdx.y % ntj) * kT;
     const int64_t c0 = int64_t(blockIdx.x) * chunk;
     const int64_t c1 = c0 + chunk < dl ? c0 + chunk : dl;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    double acc[4][4] = {};
-    double nzv[4] = {}, nxv[4] = {};
-    const bool do_nz = tj0 == 0 && tx == 0, do_nx = ti0 == 0 && ty == 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double acc[8][2] = {};
+    double nzp[4] = {}, nxp[4] = {};  // rows r0 + 16u of this thread's staging column
+    const int sr = threadIdx.x / kK, sc = threadIdx.x % kK;
 
+    // software pipeline: the next stage's 8 values are loaded into registers
+    // while the current stage feeds the tensor cores
+    double zn[4], xn[4];
+    const auto fetch = [&](int64_t kb) {
+        const int64_t k = kb + sc;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int r = sr + 16 * u;
+            zn[u] = (k < c1 && ti0 + r < n) ? __ldg(z + size_t(ti0 + r) * size_t(dl) + size_t(k)) : 0.0;
+            xn[u] = (k < c1 && tj0 + r < m) ? __ldg(x + size_t(tj0 + r) * size_t(dl) + size_t(k)) : 0.0;
+        }
+    };
+    if (c0 < c1) fetch(c0);
     for (int64_t kb = c0; kb < c1; kb += kK) {
-        // stage kK coordinates of 64 particle rows and 64 member rows
-        for (int q = threadIdx.x; q < kK * kT; q += 256) {
-            const int r = q / kK, c = q % kK;
-            const int64_t k = kb + c;
-            const int iz = ti0 + r, jx = tj0 + r;
-            zs[c][r] = (k < c1 && iz < n) ? z[size_t(iz) * size_t(dl) + size_t(k)] : 0.0;
-            xs[c][r] = (k < c1 && jx < m) ? x[size_t(jx) * size_t(dl) + size_t(k)] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int r = sr + 16 * u;
+            zs[r][sc] = zn[u];
+            xs[r][sc] = xn[u];
+            nzp[u] = fma(zn[u], zn[u], nzp[u]);
+            nxp[u] = fma(xn[u], xn[u], nxp[u]);
         }
         __syncthreads();
-#pragma unroll 4
-        for (int c = 0; c < kK; ++c) {
-            double zi[4], xj[4];  // rows ty + 16u, columns tx + 16v: conflict-free
+        if (kb + kK < c1) fetch(kb + kK);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                zi[u] = zs[c][ty + 16 * u];
-                xj[u] = xs[c][tx + 16 * u];
-            }
+        for (int kq = 0; kq < kK / 4; ++kq) {
+            const int kk = 4 * kq + (lane & 3);
+            const double a = zs[8 * warp + (lane >> 2)][kk];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) acc[u][v] = fma(zi[u], xj[v], acc[u][v]);
-            if (do_nz)
-#pragma unroll
-                for (int u = 0; u < 4; ++u) nzv[u] = fma(zi[u], zi[u], nzv[u]);
-            if (do_nx)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) nxv[v] = fma(xj[v], xj[v], nxv[v]);
+            for (int nt = 0; nt < 8; ++nt) dmma_8x8x4(acc[nt], a, xs[8 * nt + (lane >> 2)][kk]);
         }
         __syncthreads();
     }
+    // norms: the 16 threads of a half-warp share rows sr + 16u
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        for (int o = 8; o > 0; o >>= 1) {
+            nzp[u] += __shfl_xor_sync(0xffffffffu, nzp[u], o);
+            nxp[u] += __shfl_xor_sync(0xffffffffu, nxp[u], o);
+        }
     // part[chunk] = [G (n x m) | nz (n) | nx (m)]
     double* out = part + size_t(blockIdx.x) * (size_t(n) * m + n + m);
+    const int i = ti0 + 8 * warp + (lane >> 2);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int i = ti0 + ty + 16 * u;
-        if (i >= n) continue;
+    for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int j = tj0 + tx + 16 * v;
-            if (j < m) out[size_t(i) * m + j] = acc[u][v];
+        for (int e = 0; e < 2; ++e) {
+            const int j = tj0 + 8 * nt + 2 * (lane & 3) + e;
+            if (i < n && j < m) out[size_t(i) * m + j] = acc[nt][e];
         }
-        if (do_nz) out[size_t(n) * m + i] = nzv[u];
-    }
-    if (do_nx)
+    if (sc == 0)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int j = tj0 + tx + 16 * v;
-            if (j < m) out[size_t(n) * m + n + j] = nxv[v];
+        for (int u = 0; u < 4; ++u) {
+            const int r = sr + 16 * u;
+            if (tj0 == 0 && ti0 + r < n) out[size_t(n) * m + ti0 + r] = nzp[u];
+            if (ti0 == 0 && tj0 + r < m) out[size_t(n) * m + n + tj0 + r] = nxp[u];
         }
 }
 
-// red[q] = sum over chunks of part[chunk][q], in chunk order (deterministic)
+// Fixed-order (deterministic) sum over chunks: stage 1 sums chunk group
+// blockIdx.y (chunks y, y + G, y + 2G, ...) into part2[y]; stage 2 sums the
+// G groups in order.
+constexpr int kGroups = 16;
+
 __global__ void reduce_chunks_kernel(const double* __restrict__ part, int nchunk, size_t len,
+                                     double* __restrict__ part2) {
+    const size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= len) return;
+    double s = 0.0;
+    for (int c = blockIdx.y; c < nchunk; c += kGroups) s += part[size_t(c) * len + q];
+    part2[size_t(blockIdx.y) * len + q] = s;
+}
+
+__global__ void reduce_groups_kernel(const double* __restrict__ part2, size_t len,
                                      double* __restrict__ red) {
     const size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= len) return;
     double s = 0.0;
-    for (int c = 0; c < nchunk; ++c) s += part[size_t(c) * len + q];
+#pragma unroll
+    for (int g = 0; g < kGroups; ++g) s += part2[size_t(g) * len + q];
     red[q] = s;
 }
 
@@ -188,14 +220,15 @@ __global__ void joint_softmax_kernel(const double* __restrict__ red, int n, int 
 // per warp; member rows are staged through shared memory 64 at a time, so a
 // loaded x pair feeds kJP particles.  kF32Noise: the particle normals come
 // from the fp32 Box-Muller of the fast path (the update stays fp64).
-constexpr int kJP = 8, kJW = 4, kJM = 64;
+constexpr int kJP = 8, kJW = 8, kJM = 32;
 
 template <bool kF32Noise>
-__global__ void __launch_bounds__(kJW * 32) joint_apply_kernel(
+__global__ void __launch_bounds__(kJW * 32, 2) joint_apply_kernel(
     KernelArgs a, const double* __restrict__ x, const double2* __restrict__ ab,
     const double* __restrict__ wn, StepF64 c, int step, double* __restrict__ z,
     unsigned long long* __restrict__ status) {
     __shared__ double2 xs[kJM][32];
+    __shared__ double ws[kJW * kJP][kJM];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t kl = int64_t(blockIdx.x) * 64 + 2 * lane;
     const int i0 = (blockIdx.y * kJW + warp) * kJP;
@@ -219,13 +252,17 @@ __global__ void __launch_bounds__(kJW * 32) joint_apply_kernel(
                 v.x = __ldg(row + k);
             xs[jj][l] = v;
         }
+        for (int q = threadIdx.x; q < kJW * kJP * jn; q += kJW * 32) {
+            const int pp = q / jn, jj = q % jn;
+            const int i = blockIdx.y * kJW * kJP + pp;
+            ws[pp][jj] = i < a.m ? wn[size_t(i) * a.m + j0 + jj] : 0.0;
+        }
         __syncthreads();
         for (int jj = 0; jj < jn; ++jj) {
             const double2 xv = xs[jj][lane];
 #pragma unroll
             for (int p = 0; p < kJP; ++p) {
-                const int i = i0 + p < a.m ? i0 + p : a.m - 1;
-                const double w = __ldg(wn + size_t(i) * a.m + j0 + jj);  // warp-uniform
+                const double w = ws[warp * kJP + p][jj];  // broadcast
                 sx[p] = fma(w, xv.x, sx[p]);
                 sy[p] = fma(w, xv.y, sy[p]);
             }
@@ -241,8 +278,9 @@ __global__ void __launch_bounds__(kJW * 32) joint_apply_kernel(
         if (i >= a.m) break;
         double* zr = z + size_t(i) * size_t(a.dl) + kl;
         double zx = zr[0], zy = has_y ? zr[1] : 0.0;
-        double scx = -(zx - c.alpha * sx[p]) / c.beta2;
-        double scy = -(zy - c.alpha * sy[p]) / c.beta2;
+        const double ib2 = 2.0 * c.inv2b;  // 1 / beta^2
+        double scx = -(zx - c.alpha * sx[p]) * ib2;
+        double scy = -(zy - c.alpha * sy[p]) * ib2;
         if (a.obs_atan) {
             scx += c.damp * ((o0.y - o0.x * atan(zx)) / (1.0 + zx * zx));
             scy += c.damp * ((o1.y - o1.x * atan(zy)) / (1.0 + zy * zy));
@@ -279,6 +317,7 @@ JointPlan joint_plan(int n, int m, int64_t dl) {
     if (pl.nchunk < 1) pl.nchunk = 1;
     pl.tiles = tiles;
     pl.red_len = size_t(n) * m + n + m;
+    pl.scratch = (size_t(pl.nchunk) + kGroups) * pl.red_len;
     return pl;
 }
 
@@ -296,8 +335,13 @@ cudaError_t launch_joint_gram(const KernelArgs& a, const JointPlan& pl, const do
             z, x, a.m, a.m, a.dl, pl.chunk, part);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        reduce_chunks_kernel<<<unsigned((pl.red_len + 255) / 256), 256, 0, st>>>(part, pl.nchunk,
-                                                                              pl.red_len, red);
+        double* part2 = part + size_t(pl.nchunk) * pl.red_len;
+        reduce_chunks_kernel<<<dim3(unsigned((pl.red_len + 255) / 256), kGroups), 256, 0, st>>>(
+            part, pl.nchunk, pl.red_len, part2);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        reduce_groups_kernel<<<unsigned((pl.red_len + 255) / 256), 256, 0, st>>>(part2, pl.red_len,
+                                                                              red);
     } else {
         cudaMemsetAsync(red, 0, sizeof(double) * pl.red_len, st);
     }
