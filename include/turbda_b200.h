@@ -39,6 +39,12 @@ extern "C" {
 
 #define TURBDA_B200_ABI_VERSION 1
 
+#if defined(__GNUC__)
+#define TURBDA_API __attribute__((visibility("default")))
+#else
+#define TURBDA_API
+#endif
+
 typedef enum turbda_code {
     TURBDA_OK = 0,
     TURBDA_CONFIG = 1,     /* ConfigError                                  */
@@ -46,7 +52,9 @@ typedef enum turbda_code {
     TURBDA_DIVERGED = 3,   /* SamplerDivergedError(pseudo_time)            */
     TURBDA_DOMAIN = 4,     /* std::domain_error (score time outside [eps,1]) */
     TURBDA_CUDA = 5,       /* no device / CUDA runtime failure             */
-    TURBDA_INTERNAL = 6
+    TURBDA_INTERNAL = 6,
+    TURBDA_BLOWUP = 7,     /* BlowupError(time, member): SQG state non-finite */
+    TURBDA_ABORTED = 8     /* RunAbortedError(cycle): status.diverged_step  */
 } turbda_code;
 
 typedef enum turbda_precision {
@@ -116,7 +124,7 @@ typedef struct turbda_ensf_params {
 
 /* Fills *p with the reference defaults (include/turbda/ensf.hpp:22-27):
  * n_steps 100, eps 0.01, minibatch 0, damping_t 1, relax 1, fp32, device -1. */
-void turbda_ensf_params_init(turbda_ensf_params* p);
+TURBDA_API void turbda_ensf_params_init(turbda_ensf_params* p);
 
 /*
  * forecast     [n_members][d_local] row-major fp64 (member-major, like the
@@ -127,7 +135,7 @@ void turbda_ensf_params_init(turbda_ensf_params* p);
  * stream       cudaStream_t to run on; NULL = the legacy default stream in
  *              device mode, an internal per-device stream in host mode
  */
-int turbda_ensf_analyze(const turbda_ensf_params* p, const double* forecast, const double* y,
+TURBDA_API int turbda_ensf_analyze(const turbda_ensf_params* p, const double* forecast, const double* y,
                         const double* r_diag, const int64_t* obs_idx, double* analysis_out,
                         void* stream, turbda_status* status);
 
@@ -135,16 +143,16 @@ int turbda_ensf_analyze(const turbda_ensf_params* p, const double* forecast, con
  * reference's Ensemble::members layout): forecast_rows[j] and
  * analysis_rows[j] point at d_local doubles each.  Host buffers only; saves
  * the caller packing a contiguous [M][d] copy. */
-int turbda_ensf_analyze_rows(const turbda_ensf_params* p, const double* const* forecast_rows,
+TURBDA_API int turbda_ensf_analyze_rows(const turbda_ensf_params* p, const double* const* forecast_rows,
                              const double* y, const double* r_diag, const int64_t* obs_idx,
                              double* const* analysis_rows, turbda_status* status);
 
 /* After a TURBDA_ASYNC call and a synchronize of its stream: verdict of the
  * most recent analysis on `device`. */
-int turbda_ensf_check(int device, const turbda_ensf_params* p, turbda_status* status);
+TURBDA_API int turbda_ensf_check(int device, const turbda_ensf_params* p, turbda_status* status);
 
 /* relax_spread on the device; host or device buffers per `flags`. */
-int turbda_relax_spread(const double* analysis, const double* forecast, int32_t n_members,
+TURBDA_API int turbda_relax_spread(const double* analysis, const double* forecast, int32_t n_members,
                         int64_t d, double factor, double* out, int32_t device, uint32_t flags,
                         void* stream, turbda_status* status);
 
@@ -153,7 +161,7 @@ int turbda_relax_spread(const double* analysis, const double* forecast, int32_t 
  * likelihood when y != NULL (posterior_score), fp64, host buffers.
  * batch: member indices or NULL (all members).
  */
-int turbda_score(const double* z, int64_t d, double t, const double* forecast, int32_t n_members,
+TURBDA_API int turbda_score(const double* z, int64_t d, double t, const double* forecast, int32_t n_members,
                  const int32_t* batch, int32_t n_batch, double eps, const double* y,
                  const double* r_diag, const int64_t* obs_idx, int64_t obs_dim, int32_t obs_kind,
                  double damping_t, double* out, int32_t device, turbda_status* status);
@@ -161,7 +169,7 @@ int turbda_score(const double* z, int64_t d, double t, const double* forecast, i
 /* out[0] = sum_k (mean_k - truth_k)^2 (0 when truth == NULL),
  * out[1] = sum_{j,k} (x_jk - mean_k)^2.  members / truth are host or device
  * buffers per flags; out is always a host double[2]. */
-int turbda_diag(const double* members, int32_t n_members, int64_t d, const double* truth,
+TURBDA_API int turbda_diag(const double* members, int32_t n_members, int64_t d, const double* truth,
                 double* out, int32_t device, uint32_t flags, void* stream,
                 turbda_status* status);
 
@@ -173,26 +181,87 @@ int turbda_diag(const double* members, int32_t n_members, int64_t d, const doubl
  *   rank 0: turbda_comm_unique_id(id) -> broadcast the 128 bytes -> every
  *   rank: turbda_comm_init(device, rank, world, id).
  */
-int turbda_comm_unique_id(void* id128, turbda_status* status);
-int turbda_comm_init(int32_t device, int32_t rank, int32_t world, const void* id128,
+TURBDA_API int turbda_comm_unique_id(void* id128, turbda_status* status);
+TURBDA_API int turbda_comm_init(int32_t device, int32_t rank, int32_t world, const void* id128,
                      turbda_status* status);
-int turbda_comm_destroy(int32_t device);
+TURBDA_API int turbda_comm_destroy(int32_t device);
+
+/* ---------------------------------------------------------------------------
+ * Forecast model and cycle driver (the callers either side of the analysis,
+ * SURVEY.md 8(f)): a batched GPU two-boundary SQG model (fp64, cuFFT)
+ * replacing SqgStepper / nature_run (proj/src/forecast.cpp:14-75,
+ * proj/src/osse.cpp:101-135), and the GPU-resident twin experiment
+ * run_experiment (proj/src/osse.cpp:182-253).
+ * ------------------------------------------------------------------------- */
+typedef struct turbda_sqg_params { /* GridSpec + SqgParams (nz = 2)         */
+    int32_t nx, ny;
+    double lx, ly, h;
+    double f, n, u0;
+    int32_t hyper_order, reserved;
+    double hyper_efold, dt, drag_tau;
+} turbda_sqg_params;
+
+/* reference defaults: 64 x 64, lx = ly = 20 pi, h 0.3, f 1, N 10, u0 0.1,
+ * order 4, e-fold 5 h, dt 0.25 h, drag 200 h */
+TURBDA_API void turbda_sqg_params_init(turbda_sqg_params* p);
+/* a model advancing `batch` states [batch][2][ny][nx] together */
+TURBDA_API int turbda_sqg_create(const turbda_sqg_params* p, int32_t batch, int32_t device, void** handle,
+                      turbda_status* status);
+/* states (host, or device with TURBDA_INPUTS_ON_DEVICE) advanced in place by
+ * `hours` (a multiple of dt); TURBDA_BLOWUP names the first non-finite member
+ * (status.diverged_particle) and its model time (status.diverged_t) */
+TURBDA_API int turbda_sqg_advance(void* handle, double* states, double hours, uint32_t flags, void* stream,
+                       double* max_cfl, turbda_status* status);
+TURBDA_API int turbda_sqg_destroy(void* handle);
+/* nature_run: snapshots [n][2][ny][nx] into host memory */
+TURBDA_API int turbda_nature_run(const turbda_sqg_params* p, double spinup, double duration,
+                      double interval, uint64_t seed, double* snapshots, int32_t max_snaps,
+                      int32_t* n_snaps, int32_t device, turbda_status* status);
+
+#define TURBDA_VARIANT_FREE_RUN 0
+#define TURBDA_VARIANT_ENSF 2 /* (1 = letkf is not part of this build) */
+
+typedef struct turbda_experiment { /* ExperimentConfig, proj/include/turbda/osse.hpp:30-50 */
+    turbda_sqg_params sqg;
+    int32_t variant;        /* TURBDA_VARIANT_*                                   */
+    int32_t model_quality;  /* 0 perfect, 1 imperfect (inject_model_error)        */
+    int32_t cycles, ensemble_size;
+    double obs_interval, spinup_hours, clim_hours;
+    uint64_t seed;
+    double obs_r;
+    int32_t obs_thinning, obs_arctan;
+    int32_t n_steps, minibatch_j;  /* EnsfConfig                                */
+    double eps, damping_t, relax_factor;
+    int32_t precision, score_mode; /* B200 extensions (turbda_ensf_params)      */
+    int32_t me_enabled, me_ncomp;  /* ModelErrorConfig                          */
+    double me_base_amplitude;      /* <= 0: climatological RMS of the nature run */
+    double me_prob[8], me_frac[8];
+} turbda_experiment;
+
+TURBDA_API void turbda_experiment_init(turbda_experiment* e);
+/* records: [cycles][6] = cycle, time, forecast_rmse, analysis_rmse,
+ * forecast_spread, analysis_spread (CycleRecord, proj/include/turbda/osse.hpp:52-59).
+ * On TURBDA_ABORTED the records of the completed cycles are valid
+ * (*n_records of them), as run_experiment's partial_out. */
+TURBDA_API int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* records,
+                          int32_t max_records, int32_t* n_records, double* max_cfl,
+                          turbda_status* status);
 
 /* Number of CUDA devices (0 when none), library ABI version, and the name of
  * the kernel family compiled in ("sm_100a"). */
-int turbda_device_count(void);
-int turbda_abi_version(void);
-const char* turbda_build_arch(void);
+TURBDA_API int turbda_device_count(void);
+TURBDA_API int turbda_abi_version(void);
+TURBDA_API const char* turbda_build_arch(void);
 
 /* Kernel launches issued by this process since load (evidence counter). */
-uint64_t turbda_launch_count(void);
+TURBDA_API uint64_t turbda_launch_count(void);
 
 /* Live timing of the fused analysis kernel: when enabled, every analysis
  * records CUDA events on its launching stream around the ensf kernel.
  * turbda_profile_read() returns (and resets) the summed kernel milliseconds
  * and the number of timed launches since the previous read. */
-void turbda_profile_enable(int on);
-int turbda_profile_read(double* kernel_ms, uint64_t* launches);
+TURBDA_API void turbda_profile_enable(int on);
+TURBDA_API int turbda_profile_read(double* kernel_ms, uint64_t* launches);
 
 #ifdef __cplusplus
 }

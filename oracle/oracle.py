@@ -349,3 +349,62 @@ def conditioned_inputs(m, d, oracle=None, stride=0):
     ht = truth if idx is None else truth[idx]
     y = ht + o.stream_normals(99, STREAM_OBS_NOISE, 1, ht.size)
     return x, y, idx, truth
+
+
+class RefCycleOracle:
+    """The reference's cycle driver and SQG model (proj/src/{osse,config,
+    forecast,sqg,spectral}.cpp + the hot path), unmodified, built against
+    cuFFTW (oracle/ref_cycle_shim.cpp).  Needs a GPU at run time."""
+
+    kind = "reference"
+
+    def __init__(self, path=None):
+        self.path = Path(path) if path else HERE / "_ref" / "libturbda_ref_cycle.so"
+        L = self.lib = C.CDLL(str(self.path))
+        L.refc_run_experiment.restype = C.c_int
+        L.refc_run_experiment.argtypes = [C.c_char_p, C.c_int, _dp, C.c_int,
+                                          C.POINTER(C.c_int), C.c_char_p, C.c_int]
+        L.refc_sqg_advance.restype = C.c_int
+        L.refc_sqg_advance.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                       C.c_double, C.c_double, _dp, _dp, C.POINTER(C.c_double),
+                                       C.c_char_p, C.c_int]
+        L.refc_nature_run.restype = C.c_int
+        L.refc_nature_run.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                      C.c_double, C.c_double, C.c_double, C.c_uint64, _dp,
+                                      C.c_int, C.POINTER(C.c_int), C.c_char_p, C.c_int]
+
+    def run_experiment(self, config: dict, workers=0):
+        import json
+        cycles = int(config.get("cycles", 300))
+        rec = np.zeros(6 * max(cycles, 1), np.float64)
+        n = C.c_int(0)
+        msg = C.create_string_buffer(512)
+        code = self.lib.refc_run_experiment(json.dumps(config).encode(), workers, rec, cycles,
+                                            C.byref(n), msg, 512)
+        if code:
+            raise OracleError(5, msg.value.decode())
+        keys = ("cycle", "time", "forecast_rmse", "analysis_rmse", "forecast_spread",
+                "analysis_spread")
+        return [dict(zip(keys, rec[6 * q:6 * q + 6])) for q in range(n.value)]
+
+    def sqg_advance(self, state, hours, nx, ny, lx, ly, h=0.3, dt=0.25):
+        s = np.ascontiguousarray(state, np.float64).ravel()
+        out = np.empty_like(s)
+        cfl = C.c_double(0)
+        msg = C.create_string_buffer(512)
+        code = self.lib.refc_sqg_advance(nx, ny, lx, ly, h, dt, hours, s, out, C.byref(cfl), msg,
+                                         512)
+        if code:
+            raise OracleError(5, msg.value.decode())
+        return out, cfl.value
+
+    def nature_run(self, nx, ny, lx, ly, spinup, duration, interval, seed, h=0.3):
+        n_snap = int(round(duration / interval)) + 1
+        out = np.empty(n_snap * 2 * nx * ny, np.float64)
+        n = C.c_int(0)
+        msg = C.create_string_buffer(512)
+        code = self.lib.refc_nature_run(nx, ny, lx, ly, h, spinup, duration, interval, seed, out,
+                                        n_snap, C.byref(n), msg, 512)
+        if code:
+            raise OracleError(5, msg.value.decode())
+        return out.reshape(n_snap, 2 * nx * ny)[: n.value]

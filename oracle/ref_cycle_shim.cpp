@@ -1,0 +1,115 @@
+// TEST INFRASTRUCTURE ONLY - C-ABI over the reference's *unmodified* cycle
+// driver and SQG model, built with cuFFTW in place of FFTW (oracle/Makefile
+// `ref-cycle`, output oracle/_ref/libturbda_ref_cycle.so; needs a GPU at run
+// time because cuFFTW runs on cuFFT).  Entry points:
+//   refc_run_experiment -> turbda::run_experiment  proj/src/osse.cpp:182-253
+//                          (JSON config: turbda::config_from_json, proj/src/config.cpp:64-131)
+//   refc_sqg_advance    -> turbda::SqgStepper::advance proj/src/forecast.cpp:14-32
+//   refc_nature_run     -> turbda::nature_run      proj/src/osse.cpp:101-135
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include <nlohmann/json.hpp>
+
+#include "turbda/config.hpp"
+#include "turbda/forecast.hpp"
+#include "turbda/osse.hpp"
+
+namespace turbda {
+Ensemble letkf_analyze(const Ensemble&, const Observation&, const LetkfConfig&, const GridSpec&,
+                       int) {
+    throw ConfigError("letkf is not built in the cycle oracle");
+}
+}  // namespace turbda
+
+using namespace turbda;
+
+namespace {
+void put(char* msg, int len, const char* what) {
+    if (msg && len > 0) {
+        std::strncpy(msg, what, size_t(len - 1));
+        msg[len - 1] = 0;
+    }
+}
+GridSpec grid_of(int nx, int ny, double lx, double ly, double h) {
+    GridSpec g;
+    g.nx = nx;
+    g.ny = ny;
+    g.lx = lx;
+    g.ly = ly;
+    g.h = h;
+    return g;
+}
+}  // namespace
+
+extern "C" {
+
+// records: [max_records][6] = cycle, time, forecast_rmse, analysis_rmse,
+// forecast_spread, analysis_spread
+int refc_run_experiment(const char* config_json, int workers, double* records, int max_records,
+                        int* n_records, char* msg, int msglen) {
+    try {
+        const ExperimentConfig cfg = config_from_json(nlohmann::json::parse(config_json));
+        MetricsSeries partial;
+        const MetricsSeries ms = run_experiment(cfg, nullptr, {}, workers, nullptr, &partial);
+        int n = 0;
+        for (const auto& r : ms.records) {
+            if (n >= max_records) break;
+            double* o = records + 6 * n;
+            o[0] = r.cycle;
+            o[1] = r.time;
+            o[2] = r.forecast_rmse;
+            o[3] = r.analysis_rmse;
+            o[4] = r.forecast_spread;
+            o[5] = r.analysis_spread;
+            ++n;
+        }
+        *n_records = n;
+        return 0;
+    } catch (const std::exception& e) {
+        put(msg, msglen, e.what());
+        return 1;
+    }
+}
+
+int refc_sqg_advance(int nx, int ny, double lx, double ly, double h, double dt, double hours,
+                     const double* state, double* out, double* max_cfl, char* msg, int msglen) {
+    try {
+        SqgParams p;
+        p.dt = dt;
+        SqgStepper st(grid_of(nx, ny, lx, ly, h), p);
+        std::vector<double> v(state, state + size_t(2) * nx * ny);
+        st.advance(v, hours);
+        std::memcpy(out, v.data(), v.size() * sizeof(double));
+        if (max_cfl) *max_cfl = st.max_cfl();
+        return 0;
+    } catch (const std::exception& e) {
+        put(msg, msglen, e.what());
+        return 1;
+    }
+}
+
+int refc_nature_run(int nx, int ny, double lx, double ly, double h, double spinup,
+                    double duration, double interval, uint64_t seed, double* out, int max_snaps,
+                    int* n_snaps, char* msg, int msglen) {
+    try {
+        const auto snaps =
+            nature_run(grid_of(nx, ny, lx, ly, h), SqgParams{}, spinup, duration, interval, seed);
+        int n = 0;
+        for (const auto& s : snaps) {
+            if (n >= max_snaps) break;
+            std::memcpy(out + size_t(n) * s.size(), s.data(), s.size() * sizeof(double));
+            ++n;
+        }
+        *n_snaps = n;
+        return 0;
+    } catch (const std::exception& e) {
+        put(msg, msglen, e.what());
+        return 1;
+    }
+}
+
+}  // extern "C"

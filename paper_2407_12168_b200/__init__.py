@@ -10,6 +10,7 @@ the built extension fails loudly - there is no CPU fallback.
 from ._core import ConfigError, DimensionError, GridSpec, ensf_analyze  # noqa: F401
 from ._core import build_arch, device_count, launch_count  # noqa: F401
 from . import capi  # noqa: F401
+from .experiment import default_config_json, run_experiment  # noqa: F401
 
 __all__ = ["ConfigError", "DimensionError", "GridSpec", "ensf_analyze", "capi", "build_arch",
-           "device_count", "launch_count"]
+           "device_count", "launch_count", "run_experiment", "default_config_json"]

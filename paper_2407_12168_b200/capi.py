@@ -16,7 +16,8 @@ import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libturbda_b200.so"
 
-OK, CONFIG, DIMENSION, DIVERGED, DOMAIN, CUDA, INTERNAL = range(7)
+OK, CONFIG, DIMENSION, DIVERGED, DOMAIN, CUDA, INTERNAL, BLOWUP, ABORTED = range(9)
+VARIANT_FREE_RUN, VARIANT_ENSF = 0, 2
 SCORE_COMPONENTWISE, SCORE_JOINT = 0, 1
 FP32, FP64 = 0, 1
 INPUTS_ON_DEVICE = 0x1
@@ -33,6 +34,26 @@ class EnsfParams(C.Structure):
         ("device_count", C.c_int32), ("flags", C.c_uint32), ("score_mode", C.c_int32),
         ("reserved", C.c_int32),
     ]
+
+
+class SqgParams(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("lx", C.c_double), ("ly", C.c_double),
+                ("h", C.c_double), ("f", C.c_double), ("n", C.c_double), ("u0", C.c_double),
+                ("hyper_order", C.c_int32), ("reserved", C.c_int32), ("hyper_efold", C.c_double),
+                ("dt", C.c_double), ("drag_tau", C.c_double)]
+
+
+class Experiment(C.Structure):
+    _fields_ = [("sqg", SqgParams), ("variant", C.c_int32), ("model_quality", C.c_int32),
+                ("cycles", C.c_int32), ("ensemble_size", C.c_int32),
+                ("obs_interval", C.c_double), ("spinup_hours", C.c_double),
+                ("clim_hours", C.c_double), ("seed", C.c_uint64), ("obs_r", C.c_double),
+                ("obs_thinning", C.c_int32), ("obs_arctan", C.c_int32), ("n_steps", C.c_int32),
+                ("minibatch_j", C.c_int32), ("eps", C.c_double), ("damping_t", C.c_double),
+                ("relax_factor", C.c_double), ("precision", C.c_int32), ("score_mode", C.c_int32),
+                ("me_enabled", C.c_int32), ("me_ncomp", C.c_int32),
+                ("me_base_amplitude", C.c_double), ("me_prob", C.c_double * 8),
+                ("me_frac", C.c_double * 8)]
 
 
 class Status(C.Structure):
@@ -95,6 +116,25 @@ def lib() -> C.CDLL:
         L.turbda_comm_init.restype = C.c_int
         L.turbda_comm_destroy.argtypes = [C.c_int32]
         L.turbda_comm_destroy.restype = C.c_int
+        L.turbda_sqg_params_init.argtypes = [C.POINTER(SqgParams)]
+        L.turbda_sqg_params_init.restype = None
+        L.turbda_sqg_create.argtypes = [C.POINTER(SqgParams), C.c_int32, C.c_int32,
+                                        C.POINTER(C.c_void_p), C.POINTER(Status)]
+        L.turbda_sqg_create.restype = C.c_int
+        L.turbda_sqg_advance.argtypes = [C.c_void_p, vp, C.c_double, C.c_uint32, vp, dp,
+                                         C.POINTER(Status)]
+        L.turbda_sqg_advance.restype = C.c_int
+        L.turbda_sqg_destroy.argtypes = [C.c_void_p]
+        L.turbda_sqg_destroy.restype = C.c_int
+        L.turbda_nature_run.argtypes = [C.POINTER(SqgParams), C.c_double, C.c_double, C.c_double,
+                                        C.c_uint64, vp, C.c_int32, C.POINTER(C.c_int32),
+                                        C.c_int32, C.POINTER(Status)]
+        L.turbda_nature_run.restype = C.c_int
+        L.turbda_experiment_init.argtypes = [C.POINTER(Experiment)]
+        L.turbda_experiment_init.restype = None
+        L.turbda_run_experiment.argtypes = [C.POINTER(Experiment), C.c_int32, vp, C.c_int32,
+                                            C.POINTER(C.c_int32), dp, C.POINTER(Status)]
+        L.turbda_run_experiment.restype = C.c_int
         _lib = L
     return _lib
 
@@ -226,6 +266,77 @@ def comm_init(device: int, rank: int, world: int, uid: bytes) -> None:
 
 def comm_destroy(device: int) -> None:
     lib().turbda_comm_destroy(device)
+
+
+def sqg_params(**kw) -> SqgParams:
+    p = SqgParams()
+    lib().turbda_sqg_params_init(C.byref(p))
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+class SqgModel:
+    """Batched GPU SQG stepper (turbda_sqg_*): advance(states, hours) on an
+    (batch, 2, ny, nx) float64 numpy array, in place."""
+
+    def __init__(self, batch=1, device=-1, **params):
+        self.p = sqg_params(**params)
+        self.batch = batch
+        self.h = C.c_void_p()
+        st = Status()
+        _check(lib().turbda_sqg_create(C.byref(self.p), batch, device, C.byref(self.h),
+                                       C.byref(st)), st)
+        self.max_cfl = 0.0
+
+    def advance(self, states, hours):
+        a = np.ascontiguousarray(states, np.float64)
+        cfl = C.c_double(self.max_cfl)
+        st = Status()
+        _check(lib().turbda_sqg_advance(self.h, a.ctypes.data, hours, 0, None, C.byref(cfl),
+                                        C.byref(st)), st)
+        self.max_cfl = cfl.value
+        return a
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value:
+            lib().turbda_sqg_destroy(self.h)
+            self.h = C.c_void_p()
+
+
+def nature_run(spinup, duration, interval, seed, device=-1, **params):
+    p = sqg_params(**params)
+    n = int(round(duration / interval)) + 1
+    out = np.empty((n, 2 * p.nx * p.ny), np.float64)
+    got = C.c_int32(0)
+    st = Status()
+    _check(lib().turbda_nature_run(C.byref(p), spinup, duration, interval, seed,
+                                   out.ctypes.data, n, C.byref(got), device, C.byref(st)), st)
+    return out[: got.value]
+
+
+def experiment(**kw) -> Experiment:
+    e = Experiment()
+    lib().turbda_experiment_init(C.byref(e))
+    for k, v in kw.items():
+        setattr(e, k, v)
+    return e
+
+
+def run_experiment_raw(e: Experiment, device=-1):
+    """(records [n][6], max_cfl); raises TurbdaError (records of completed
+    cycles in err.partial on TURBDA_ABORTED)."""
+    rec = np.zeros((max(e.cycles, 1), 6), np.float64)
+    n = C.c_int32(0)
+    cfl = C.c_double(0)
+    st = Status()
+    code = lib().turbda_run_experiment(C.byref(e), device, rec.ctypes.data, e.cycles,
+                                       C.byref(n), C.byref(cfl), C.byref(st))
+    if code != OK:
+        err = TurbdaError(code, st)
+        err.partial = rec[: n.value]
+        raise err
+    return rec[: n.value], cfl.value
 
 
 def device_count() -> int:
