@@ -242,10 +242,13 @@ TURBDA_API void turbda_experiment_init(turbda_experiment* e);
 /* records: [cycles][6] = cycle, time, forecast_rmse, analysis_rmse,
  * forecast_spread, analysis_spread (CycleRecord, proj/include/turbda/osse.hpp:52-59).
  * On TURBDA_ABORTED the records of the completed cycles are valid
- * (*n_records of them), as run_experiment's partial_out. */
+ * (*n_records of them), as run_experiment's partial_out.
+ * phase_seconds (optional, [4]): device time of the nature run + truth bundle,
+ * all ensemble forecasts (+ model error), all analyses (+ observation
+ * synthesis), all diagnostics. */
 TURBDA_API int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* records,
                           int32_t max_records, int32_t* n_records, double* max_cfl,
-                          turbda_status* status);
+                          double* phase_seconds, turbda_status* status);
 
 /* Number of CUDA devices (0 when none), library ABI version, and the name of
  * the kernel family compiled in ("sm_100a"). */

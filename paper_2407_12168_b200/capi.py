@@ -133,7 +133,7 @@ def lib() -> C.CDLL:
         L.turbda_experiment_init.argtypes = [C.POINTER(Experiment)]
         L.turbda_experiment_init.restype = None
         L.turbda_run_experiment.argtypes = [C.POINTER(Experiment), C.c_int32, vp, C.c_int32,
-                                            C.POINTER(C.c_int32), dp, C.POINTER(Status)]
+                                            C.POINTER(C.c_int32), dp, vp, C.POINTER(Status)]
         L.turbda_run_experiment.restype = C.c_int
         _lib = L
     return _lib
@@ -323,15 +323,18 @@ def experiment(**kw) -> Experiment:
     return e
 
 
-def run_experiment_raw(e: Experiment, device=-1):
+def run_experiment_raw(e: Experiment, device=-1, phases=None):
     """(records [n][6], max_cfl); raises TurbdaError (records of completed
-    cycles in err.partial on TURBDA_ABORTED)."""
+    cycles in err.partial on TURBDA_ABORTED).  ``phases``: optional float64[4]
+    receiving the device seconds of nature run / forecasts / analyses / diagnostics."""
     rec = np.zeros((max(e.cycles, 1), 6), np.float64)
     n = C.c_int32(0)
     cfl = C.c_double(0)
     st = Status()
     code = lib().turbda_run_experiment(C.byref(e), device, rec.ctypes.data, e.cycles,
-                                       C.byref(n), C.byref(cfl), C.byref(st))
+                                       C.byref(n), C.byref(cfl),
+                                       None if phases is None else phases.ctypes.data,
+                                       C.byref(st))
     if code != OK:
         err = TurbdaError(code, st)
         err.partial = rec[: n.value]

@@ -380,9 +380,11 @@ void turbda_experiment_init(turbda_experiment* e) {
 
 int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* records,
                           int32_t max_records, int32_t* n_records, double* max_cfl,
-                          turbda_status* st) {
+                          double* phase_seconds, turbda_status* st) {
     clear(st);
     *n_records = 0;
+    if (phase_seconds)
+        for (int q = 0; q < 4; ++q) phase_seconds[q] = 0.0;
     // ExperimentConfig::validate, proj/src/osse.cpp:40-62
     if (int rc = validate_sqg(&e->sqg, st)) return rc;
     if (e->variant != TURBDA_VARIANT_ENSF && e->variant != TURBDA_VARIANT_FREE_RUN)
@@ -427,6 +429,26 @@ int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* re
     const int64_t d = int64_t(2) * cfg.nx * cfg.ny;
     const int m = e->ensemble_size;
     double cfl = 0.0;
+    // phase timing with events on the driver stream
+    cudaEvent_t ev_a, ev_b;
+    CY_CUDA(cudaEventCreate(&ev_a));
+    CY_CUDA(cudaEventCreate(&ev_b));
+    struct EventGuard {
+        cudaEvent_t a, b;
+        ~EventGuard() {
+            cudaEventDestroy(a);
+            cudaEventDestroy(b);
+        }
+    } eguard{ev_a, ev_b};
+    const auto tic = [&]() { cudaEventRecord(ev_a, s); };
+    const auto toc = [&](int phase) {
+        cudaEventRecord(ev_b, s);
+        cudaEventSynchronize(ev_b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev_a, ev_b);
+        if (phase_seconds) phase_seconds[phase] += 1e-3 * ms;
+    };
+    tic();
 
     // truth bundle (make_truth_bundle, proj/src/osse.cpp:137-153)
     const double duration = e->clim_hours + e->obs_interval * double(e->cycles + 1);
@@ -435,6 +457,7 @@ int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* re
     if (int rc = nature_run_device(&e->sqg, e->spinup_hours, duration, e->obs_interval, e->seed,
                                    snaps, &n_snap, &cfl, s, st))
         return rc;
+    toc(0);
     const double* clim = snaps.as<double>();
     const double* truth = clim + size_t(n_clim) * size_t(d);  // truth[k], k = 0..cycles
     double base = e->me_base_amplitude;
@@ -543,6 +566,7 @@ int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* re
         double* rec = records + 6 * size_t(k - 1);
         int blown = -1;
         double bh = 0.0;
+        tic();
         const std::string err = model.advance(ens.as<double>(), e->obs_interval, s, &cfl, &blown, &bh);
         if (!err.empty()) return aborted(k, err);
         if (blown >= 0) {
@@ -556,13 +580,17 @@ int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* re
                                                            dfrac.as<double>(), base);
             CY_CUDA(cudaGetLastError());
         }
+        toc(1);
         const double* tk = truth + size_t(k) * size_t(d);
         double frm = 0, fsp = 0, arm = 0, asp = 0;
+        tic();
         if (int rc = metrics(ens.as<double>(), tk, &frm, &fsp)) return rc;
+        toc(3);
         if (e->variant == TURBDA_VARIANT_FREE_RUN) {
             arm = frm;
             asp = fsp;
         } else {
+            tic();
             synth_obs_kernel<<<unsigned((nobs + 255) / 256), 256, 0, s>>>(
                 tk, didx.as<int64_t>(), nobs, e->obs_arctan, sd, uint32_t(obs_key),
                 uint32_t(obs_key >> 32), uint64_t(k), dy.as<double>());
@@ -572,8 +600,11 @@ int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* re
             const int rc = turbda_ensf_analyze(&ap, ens.as<double>(), dy.as<double>(), dr.as<double>(),
                                                didx.as<int64_t>(), ens_out.as<double>(), s, &ast);
             if (rc != TURBDA_OK) return aborted(k, ast.msg);
+            toc(2);
             std::swap(ens.p, ens_out.p);
+            tic();
             if (int rc2 = metrics(ens.as<double>(), tk, &arm, &asp)) return rc2;
+            toc(3);
         }
         if (k <= max_records) {
             rec[0] = k;

@@ -94,11 +94,13 @@ def to_struct(cfg: dict) -> "capi.Experiment":
     return e
 
 
-def run_experiment(config_json: str, device: int = -1) -> list[dict]:
-    """One twin experiment; per-cycle metrics as the reference binding returns them."""
+def run_experiment(config_json: str, device: int = -1, phases=None) -> list[dict]:
+    """One twin experiment; per-cycle metrics as the reference binding returns them.
+    ``phases``: optional numpy float64[4] receiving device seconds spent in the
+    nature run, the forecasts, the analyses and the diagnostics."""
     e = to_struct(json.loads(config_json))
     try:
-        rec, _ = capi.run_experiment_raw(e, device)
+        rec, _ = capi.run_experiment_raw(e, device, phases)
     except capi.TurbdaError as err:
         if err.code == capi.CONFIG:
             raise ConfigError(str(err)) from err
