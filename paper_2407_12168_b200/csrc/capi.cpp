@@ -410,6 +410,7 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
     a.key1 = uint32_t(key >> 32);
     a.cycle_lo = uint32_t(p->cycle);  // entity = (cycle << 32) | i
     a.obs_atan = obs_arctan(p->obs_kind) ? 1 : 0;
+    a.rk = philox_round_keys(a.key0, a.key1);
 
     ProfPair prof;
     if (g_profile.load() && on_dev) {
@@ -657,6 +658,7 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
     a.key1 = uint32_t(key >> 32);
     a.cycle_lo = uint32_t(p->cycle);
     a.obs_atan = obs_arctan(p->obs_kind) ? 1 : 0;
+    a.rk = philox_round_keys(a.key0, a.key1);
     double* z = w->z.as<double>();
     TB_CUDA(launch_joint_init(a, z, s));
     ProfPair prof;

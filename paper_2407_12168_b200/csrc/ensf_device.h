@@ -6,6 +6,8 @@
 
 #include <cuda_runtime.h>
 
+#include "philox_keys.h"
+
 namespace tb200 {
 
 // Per pseudo-time step coefficients of the fp32 fast kernel (32 B).  All are
@@ -40,6 +42,7 @@ struct KernelArgs {
     uint32_t key0, key1;  // Philox key of the ensf_particles stream
     uint32_t cycle_lo;    // entity = (cycle << 32) | i  ->  hi word
     int32_t obs_atan;     // 1: h(x) = atan(x) (obs kinds 2, 3), 0: linear
+    PhiloxKeys rk;        // round keys of (key0, key1)
 };
 
 // observation operator kinds of the C-ABI (include/turbda_b200.h)

@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kProducer ? 256 + 32 * kProducerWarps : 256, k
                 const uint64_t n0 = uint64_t(s + 1) * uint64_t(a.d_total) +
                                     uint64_t(a.k0 + tile0 + 2 * l);
                 const int i = (blockIdx.y * nwarps + w) * P + p;
-                dst[q] = normal_pair_f32(n0, uint32_t(i), a.cycle_lo, a.key0, a.key1);
+                dst[q] = normal_pair_f32(n0, uint32_t(i), a.cycle_lo, a.rk);
             }
             bar_arrive(1 + b, blockDim.x);  // buffer b holds step s
         }
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kProducer ? 256 + 32 * kProducerWarps : 256, k
     int bad[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
-        z[p] = normal_pair_f32(kg, uint32_t(i0 + p), a.cycle_lo, a.key0, a.key1);
+        z[p] = normal_pair_f32(kg, uint32_t(i0 + p), a.cycle_lo, a.rk);
         bad[p] = INT_MAX;
     }
 
@@ -340,8 +340,7 @@ __global__ void __launch_bounds__(kProducer ? 256 + 32 * kProducerWarps : 256, k
                 lik = __ffma2_rn(nA2, z[p], B2);
             }
             const float2 xi = kProducer ? xin[p * 32]
-                                        : normal_pair_f32(n0, uint32_t(i0 + p), a.cycle_lo,
-                                                          a.key0, a.key1);
+                                        : normal_pair_f32(n0, uint32_t(i0 + p), a.cycle_lo, a.rk);
             float2 zn = __ffma2_rn(z[p], f2(c.nbdt), z[p]);
             zn = __ffma2_rn(f2(c.kp), q, zn);
             zn = __ffma2_rn(f2(c.kl), lik, zn);
@@ -776,6 +775,13 @@ cudaError_t launch_ensf_f32(const KernelArgs& a, const double* x, const double2*
     const auto warps_for = [&](int pp) { return tiles_n * ((a.m + pp - 1) / pp); };
     const int64_t wave = 148 * 24;
     // (particles past m in the last warp are computed and discarded)
+    static const int forced_p = [] {
+        const char* e = std::getenv("TURBDA_F32_P");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced_p == 4) return launch_f32_p<4>(a, xt, ab, steps, batches, z, status, st, sorted);
+    if (forced_p == 2) return launch_f32_p<2>(a, xt, ab, steps, batches, z, status, st, sorted);
+    if (forced_p == 1) return launch_f32_p<1>(a, xt, ab, steps, batches, z, status, st, sorted);
     if ((a.m % 4 == 0 || a.m >= 32) && warps_for(4) >= wave)
         return launch_f32_p<4>(a, xt, ab, steps, batches, z, status, st, sorted);
     if ((a.m % 2 == 0 || a.m >= 16) && warps_for(2) >= wave / 2)

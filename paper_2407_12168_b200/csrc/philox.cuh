@@ -11,6 +11,8 @@
 #pragma once
 #include <cstdint>
 
+#include "philox_keys.h"
+
 namespace tb200 {
 
 struct PhiloxOut {
@@ -32,6 +34,21 @@ __device__ __forceinline__ PhiloxOut philox_block(uint64_t q, uint32_t e_lo, uin
         c3 = uint32_t(p0);
         k0 += 0x9E3779B9u;
         k1 += 0xBB67AE85u;
+    }
+    return {c0, c1, c2, c3};
+}
+
+__device__ __forceinline__ PhiloxOut philox_block_rk(uint64_t q, uint32_t e_lo, uint32_t e_hi,
+                                                     const PhiloxKeys& rk) {
+    uint32_t c0 = uint32_t(q), c1 = uint32_t(q >> 32), c2 = e_lo, c3 = e_hi;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = uint64_t(c0) * 0xD2511F53u;
+        const uint64_t p1 = uint64_t(c2) * 0xCD9E8D57u;
+        c0 = uint32_t(p1 >> 32) ^ c1 ^ rk.k[2 * r];
+        c2 = uint32_t(p0 >> 32) ^ c3 ^ rk.k[2 * r + 1];
+        c1 = uint32_t(p1);
+        c3 = uint32_t(p0);
     }
     return {c0, c1, c2, c3};
 }
@@ -85,6 +102,14 @@ __device__ __forceinline__ float2 normal_pair_f32(uint64_t n0, uint32_t e_lo, ui
     if ((n0 & 1u) == 0) return box_muller_f32(philox_block(n0 >> 1, e_lo, e_hi, k0, k1));
     const float2 a = box_muller_f32(philox_block(n0 >> 1, e_lo, e_hi, k0, k1));
     const float2 b = box_muller_f32(philox_block((n0 >> 1) + 1, e_lo, e_hi, k0, k1));
+    return make_float2(a.y, b.x);
+}
+
+__device__ __forceinline__ float2 normal_pair_f32(uint64_t n0, uint32_t e_lo, uint32_t e_hi,
+                                                  const PhiloxKeys& rk) {
+    if ((n0 & 1u) == 0) return box_muller_f32(philox_block_rk(n0 >> 1, e_lo, e_hi, rk));
+    const float2 a = box_muller_f32(philox_block_rk(n0 >> 1, e_lo, e_hi, rk));
+    const float2 b = box_muller_f32(philox_block_rk((n0 >> 1) + 1, e_lo, e_hi, rk));
     return make_float2(a.y, b.x);
 }
 
