@@ -152,24 +152,9 @@ __device__ __forceinline__ float sort_key(float v) { return v != v ? __int_as_fl
 // coordinate, proj/src/ensf.cpp:43-61), pass 1 becomes a binary search.
 // kPolyEvery: every kPolyEvery-th (member, particle) slot of the unrolled
 // member loop takes its two exponentials from ex2_poly2 instead of MUFU.
-// kProducer: two extra "noise" warps per CTA generate the Philox/Box-Muller
-// normals of every particle of the CTA one or two pseudo-steps ahead into a
-// double-buffered shared array (named barriers 1-4 hand the buffers over), so
-// the consumer warps' MUFU-bound member loop never stops for the
-// latency-bound integer Philox chains.
-constexpr int kProducerWarps = 2;
-
-__device__ __forceinline__ void bar_sync(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bar_arrive(int id, int n) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
 template <int P, bool kMinibatch, bool kSorted, int kPolyEvery, int kMinBlocks = 1,
-          bool kGlobalX = false, bool kProducer = false>
-__global__ void __launch_bounds__(kProducer ? 256 + 32 * kProducerWarps : 256, kMinBlocks)
-    ensf_f32_kernel(KernelArgs a, const float* __restrict__ xt,
+          bool kGlobalX = false>
+__global__ void __launch_bounds__(256, kMinBlocks) ensf_f32_kernel(KernelArgs a, const float* __restrict__ xt,
                                                        const double2* __restrict__ ab,
                                                        const StepF32* __restrict__ steps,
                                                        const int32_t* __restrict__ batches,
@@ -189,13 +174,10 @@ __global__ void __launch_bounds__(kProducer ? 256 + 32 * kProducerWarps : 256, k
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int nwarps = (blockDim.x >> 5) - (kProducer ? kProducerWarps : 0);  // consumer warps
+    const int nwarps = blockDim.x >> 5;
     const int64_t tile0 = int64_t(blockIdx.x) * kTile;
     const int64_t kl = tile0 + 2 * lane;  // local coordinate of this lane's pair
     const bool aligned = ((a.dl & 1) == 0);
-    // [2][nwarps][P][32] noise pairs (kProducer)
-    float2* xib = reinterpret_cast<float2*>(reinterpret_cast<float*>(cs + a.n_steps) +
-                                            (kGlobalX ? 0 : size_t(a.m) * kTile));
 
     for (int q = threadIdx.x; q < a.n_steps; q += blockDim.x) cs[q] = steps[q];
     if (!kGlobalX) {
@@ -222,25 +204,6 @@ __global__ void __launch_bounds__(kProducer ? 256 + 32 * kProducerWarps : 256, k
     int top = 1;
     while (top * 2 <= a.j_batch) top *= 2;
     __syncthreads();
-
-    if (kProducer && warp >= nwarps) {
-        const int pt = threadIdx.x - nwarps * 32;
-        const int per_step = nwarps * P * 32;
-        for (int s = 0; s < a.n_steps; ++s) {
-            const int b = s & 1;
-            if (s >= 2) bar_sync(3 + b, blockDim.x);  // consumers released buffer b
-            float2* dst = xib + size_t(b) * per_step;
-            for (int q = pt; q < per_step; q += 32 * kProducerWarps) {
-                const int l = q & 31, p = (q >> 5) % P, w = (q >> 5) / P;
-                const uint64_t n0 = uint64_t(s + 1) * uint64_t(a.d_total) +
-                                    uint64_t(a.k0 + tile0 + 2 * l);
-                const int i = (blockIdx.y * nwarps + w) * P + p;
-                dst[q] = normal_pair_f32(n0, uint32_t(i), a.cycle_lo, a.rk);
-            }
-            bar_arrive(1 + b, blockDim.x);  // buffer b holds step s
-        }
-        return;
-    }
 
     const int i0 = (blockIdx.y * nwarps + warp) * P;
     const uint64_t kg = uint64_t(a.k0 + kl);  // global coordinate of the pair's first entry
@@ -325,8 +288,6 @@ __global__ void __launch_bounds__(kProducer ? 256 + 32 * kProducerWarps : 256, k
         }
         // posterior score + Euler-Maruyama, proj/src/ensf.cpp:197-214
         const uint64_t n0 = uint64_t(s + 1) * uint64_t(a.d_total) + kg;
-        const float2* xin = xib + size_t(s & 1) * (nwarps * P * 32) + (warp * P) * 32 + lane;
-        if (kProducer) bar_sync(1 + (s & 1), blockDim.x);  // step s noise is in place
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             const float2 q = make_float2(__fdividef(num[p].x, den[p].x),
@@ -339,8 +300,7 @@ __global__ void __launch_bounds__(kProducer ? 256 + 32 * kProducerWarps : 256, k
             } else {
                 lik = __ffma2_rn(nA2, z[p], B2);
             }
-            const float2 xi = kProducer ? xin[p * 32]
-                                        : normal_pair_f32(n0, uint32_t(i0 + p), a.cycle_lo, a.rk);
+            const float2 xi = normal_pair_f32(n0, uint32_t(i0 + p), a.cycle_lo, a.rk);
             float2 zn = __ffma2_rn(z[p], f2(c.nbdt), z[p]);
             zn = __ffma2_rn(f2(c.kp), q, zn);
             zn = __ffma2_rn(f2(c.kl), lik, zn);
@@ -349,7 +309,6 @@ __global__ void __launch_bounds__(kProducer ? 256 + 32 * kProducerWarps : 256, k
             const bool fin = (fabsf(zn.x) <= FLT_MAX) && (fabsf(zn.y) <= FLT_MAX || !has_y);
             if (!fin && bad[p] == INT_MAX) bad[p] = s;
         }
-        if (kProducer && s + 2 < a.n_steps) bar_arrive(3 + (s & 1), blockDim.x);
     }
 
 #pragma unroll
@@ -665,8 +624,8 @@ bool f32_members_global(int m, int n_steps) {
     return sizeof(StepF32) * size_t(n_steps) + sizeof(float) * 64 * size_t(m) > 200 * 1024;
 }
 
-// fp32 kernel variant (sorted members / MUFU-polynomial split); the default is
-// the fastest measured, TURBDA_F32_VARIANT overrides it for experiments.
+// fp32 kernel variant for experiments (TURBDA_F32_VARIANT): 0 default,
+// 1 MUFU/FMA-polynomial exp split, 2 never sort, 3 always sort.
 int f32_variant() {
     static const int v = [] {
         const char* e = std::getenv("TURBDA_F32_VARIANT");
@@ -686,10 +645,8 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
     const dim3 grid(unsigned((a.dl + kTile - 1) / kTile), unsigned((groups + nw - 1) / nw));
     const bool global_x = f32_members_global(a.m, a.n_steps);
     const int variant = f32_variant();
-    const bool producer = sorted && !a.minibatch && !global_x && (variant == 6 || variant == 7);
     const size_t smem = sizeof(StepF32) * size_t(a.n_steps) +
-                        (global_x ? 0 : sizeof(float2) * 32 * size_t(a.m)) +
-                        (producer ? sizeof(float2) * 2 * 32 * size_t(nw) * P : 0);
+                        (global_x ? 0 : sizeof(float2) * 32 * size_t(a.m));
     // 3 CTAs of 256 threads per SM (<= 85 registers): measured best; letting
     // ptxas take more registers (1 CTA/SM) loses ~20%
     auto kern = global_x ? (a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3, true>
@@ -697,16 +654,13 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
                 : a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3>
                 : !sorted   ? ensf_f32_kernel<P, false, false, 0, 3>
                 : variant == 1 ? ensf_f32_kernel<P, false, true, 8, 3>
-                : variant == 6 ? ensf_f32_kernel<P, false, true, 0, 2, false, true>
-                : variant == 7 ? ensf_f32_kernel<P, false, true, 0, 3, false, true>
                                : ensf_f32_kernel<P, false, true, 0, 3>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(smem));
         if (e != cudaSuccess) return e;
     }
-    const dim3 blk(producer ? block.x + 32 * kProducerWarps : block.x);
-    kern<<<grid, blk, smem, st>>>(a, xt, ab, steps, batches, z, status);
+    kern<<<grid, block, smem, st>>>(a, xt, ab, steps, batches, z, status);
     return cudaGetLastError();
 }
 
@@ -755,7 +709,11 @@ cudaError_t launch_ensf_f32(const KernelArgs& a, const double* x, const double2*
                             unsigned long long* status, cudaStream_t st) {
     if (a.dl <= 0) return cudaSuccess;
     const unsigned tiles = unsigned((a.dl + kTile - 1) / kTile);
-    const bool sorted = !a.minibatch && f32_variant() != 2 && !f32_members_global(a.m, a.n_steps);
+    // sorted tiles + binary-searched shift pay off past ~24 members; below,
+    // the brute-force min pass is cheaper (measured, configs 1 and 3)
+    const int variant = f32_variant();
+    const bool sorted = !a.minibatch && variant != 2 && (a.j_batch > 24 || variant == 3) &&
+                        !f32_members_global(a.m, a.n_steps);
     const size_t smem = sizeof(float) * size_t(a.m) * kTile;
     if (sorted) {
         if (smem > 48 * 1024) {

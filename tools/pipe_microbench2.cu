@@ -32,6 +32,11 @@ __global__ void kern(float* out, long long* cyc, float seed) {
       if (OP == 8) { a[c] = fmaf(a[c], 0.999f, b[c]); }                       // FFMA imm
       if (OP == 9) { u[c] = u[c] ^ (v[c] >> 3) ^ 0x1234u; v[c] += u[c]; }    // LOP3 + IADD
       if (OP == 10) { a[c] = __fmul_rn(a[c], b[c]); b[c] = __fadd_rn(b[c], a[(c+1)%CH]); } // FMUL + FADD
+      if (OP == 11) { a[c] = ex2(a[c]); unsigned long long w = (unsigned long long)u[c] * 0xD2511F53u; u[c] = (unsigned)(w >> 32) ^ v[c]; v[c] = (unsigned)w; } // MUFU + IMAD.WIDE + LOP3
+      if (OP == 12) { a[c] = ex2(a[c]); u[c] = (u[c] ^ (v[c] >> 3)) + 0x1234u; v[c] ^= u[c]; } // MUFU + 3 ALU
+      if (OP == 14) { a[c] = ex2(a[c]); b[c] = ex2(b[c]); } // 2 independent MUFU chains
+      if (OP == 15) { a[c] = ex2(a[c]); b[c] = ex2(b[c]); p[c] = __ffma2_rn(p[c], k2, c2); } // 2 MUFU + FFMA2
+      if (OP == 13) { a[c] = ex2(a[c]); p[c] = __ffma2_rn(p[c], k2, c2); b[c] = ex2(b[c]); p[(c+1)%CH] = __fadd2_rn(p[(c+1)%CH], k2); } // 2 MUFU + FFMA2 + FADD2
     }
   }
   long long t1 = clock64();
@@ -61,5 +66,10 @@ int main() {
   run<3>("FMNMX+FFMA(x0)", 2); run<4>("MUFU.EX2", 1); run<5>("IMAD.WIDE+LOP3(2)", 2);
   run<6>("IMAD.HI+LOP+IMAD", 3); run<7>("FFMA2+MUFU", 2); run<9>("LOP3+SHF+IADD", 3);
   run<10>("FMUL+FADD", 2);
+  run<11>("MUFU+IMAD.WIDE+LOP3", 3);
+  run<12>("MUFU+3ALU", 4);
+  run<13>("2MUFU+FFMA2+FADD2", 4);
+  run<14>("2 MUFU chains", 2);
+  run<15>("2 MUFU + FFMA2", 3);
   return 0;
 }
