@@ -160,7 +160,7 @@ def reference_rate(x, y, idx, n_steps, steps, warmup):
             "ms_per_step": 1e3 * total / steps}
 
 
-def run_reference_arm(args, cfg):
+def run_reference_arm(args, cfg, json_out=None):
     """--impl reference: rank 0 times the reference's CPU implementation."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -181,10 +181,20 @@ def run_reference_arm(args, cfg):
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=json_out or sys.stdout, flush=True)
+
+
+def _json_stdout():
+    """The one JSON line goes to the original stdout; everything else written
+    to fd 1 afterwards (NCCL's version banner, library prints) goes to stderr."""
+    out = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
+    return out
 
 
 def main():
+    json_out = _json_stdout()
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -203,7 +213,7 @@ def main():
         ap.error("--warmup must be >= 3")
 
     if args.impl == "reference":
-        run_reference_arm(args, args.config)
+        run_reference_arm(args, args.config, json_out)
         return
 
     import torch
@@ -409,7 +419,7 @@ def main():
         cb = reference_rate(xs, ys, idxs, s, 1, 0)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=json_out, flush=True)
     if joint and world > 1:
         capi.comm_destroy(local)
     if world > 1:

@@ -295,8 +295,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) ensf_f32_kernel(KernelArgs a,
             float2 lik;
             if (a.obs_atan) {
                 // h(z) = atan(z): H'^T R^-1 (y - h) = (B - A atan z) / (1 + z^2)
-                lik.x = fmaf(nA2.x, atanf(z[p].x), B2.x) / fmaf(z[p].x, z[p].x, 1.f);
-                lik.y = fmaf(nA2.y, atanf(z[p].y), B2.y) / fmaf(z[p].y, z[p].y, 1.f);
+                lik.x = __fdividef(fmaf(nA2.x, atanf(z[p].x), B2.x), fmaf(z[p].x, z[p].x, 1.f));
+                lik.y = __fdividef(fmaf(nA2.y, atanf(z[p].y), B2.y), fmaf(z[p].y, z[p].y, 1.f));
             } else {
                 lik = __ffma2_rn(nA2, z[p], B2);
             }

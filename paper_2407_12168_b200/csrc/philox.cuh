@@ -88,8 +88,9 @@ __device__ __forceinline__ float u2_f32(uint32_t hi) {
 __device__ __forceinline__ float2 box_muller_f32(const PhiloxOut& w) {
     const float u1 = u1_f32(w.w0, w.w1);
     const float u2 = u2_f32(w.w3);
-    // -2 ln u1 = -2 ln2 * log2(u1)
-    const float r = sqrtf(-1.3862943611198906f * __log2f(u1));
+    // -2 ln u1 = -2 ln2 * log2(u1); MUFU.SQRT (no IEEE slow path)
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-1.3862943611198906f * __log2f(u1)));
     float s, c;
     __sincosf(6.283185307179586f * u2, &s, &c);
     return make_float2(r * c, r * s);
