@@ -70,6 +70,24 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.path = None
+        self.nvml_rows = []
+
+    def sample_now(self):
+        """One NVML sample, taken while queued timed work is still running
+        (covers timed regions shorter than nvidia-smi's start-up)."""
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            flags = ["Active" if rs & b else "Not Active" for b in bits]
+            self.nvml_rows.append([str(self.gpu), str(sm), str(mx), "", ""] + flags)
+        except Exception:  # noqa: BLE001 - sampling is best effort
+            pass
 
     def __enter__(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
@@ -100,6 +118,7 @@ class ClockSampler:
         except OSError:
             pass
         finally:
+            rows += self.nvml_rows
             if self.path:
                 try:
                     os.unlink(self.path)
@@ -295,11 +314,14 @@ def main():
                 evs[q][0].record(stream)
                 one(q)
                 evs[q][1].record(stream)
+                if q == args.steps - 1:
+                    clocks.sample_now()
         else:
             evs[0][0].record(stream)
             for q in range(args.steps):
                 one(q)
             evs[0][1].record(stream)
+            clocks.sample_now()
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
