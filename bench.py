@@ -375,7 +375,10 @@ def main():
     e2e_value = units_per_gpu * world / float(e2e_s[0])
     if stride > 1 and k0 != 0:
         pass  # the e2e leg analyses each rank's shard as its own state (same cost)
-    h2d = x0.nbytes + y0.nbytes * (3 if stride > 1 else 2)  # x, y, r (+ idx)
+    if joint and world > 1:
+        h2d = x0.nbytes + y0.nbytes * (3 if stride > 1 else 2)  # x, y, r (+ idx)
+    else:
+        h2d = x0.nbytes + y0.nbytes * (2 if stride > 1 else 1) + 8  # x, y (+ idx), one r
     d2h = res.nbytes + 8
 
     # --- roofline of the fused analysis kernel -------------------------------

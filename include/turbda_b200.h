@@ -67,6 +67,11 @@ typedef enum turbda_precision {
 #define TURBDA_ASYNC 0x2u            /* device mode only: do not synchronize;     */
                                      /* fetch the divergence verdict later with   */
                                      /* turbda_ensf_check()                       */
+#define TURBDA_R_UNIFORM 0x4u        /* r_diag points to ONE error variance used  */
+                                     /* for every observation (the scalar `r` of  */
+                                     /* the Python binding, bindings/python/      */
+                                     /* core.cpp); host or device pointer as the  */
+                                     /* other arrays                              */
 
 typedef struct turbda_status {
     int32_t code;              /* turbda_code                                   */
@@ -106,7 +111,8 @@ typedef struct turbda_ensf_params {
     int32_t device;       /* first CUDA device; -1 = current device              */
     int32_t device_count; /* >1 (host buffers only): split the window over       */
                           /* devices device .. device + device_count - 1         */
-    uint32_t flags;       /* TURBDA_INPUTS_ON_DEVICE | TURBDA_ASYNC              */
+    uint32_t flags;       /* TURBDA_INPUTS_ON_DEVICE | TURBDA_ASYNC |            */
+                          /* TURBDA_R_UNIFORM                                     */
     int32_t score_mode;   /* TURBDA_SCORE_COMPONENTWISE (the reference) or        */
                           /* TURBDA_SCORE_JOINT (north-star extension, fp64)      */
     int32_t reserved;

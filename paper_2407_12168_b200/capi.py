@@ -22,6 +22,7 @@ SCORE_COMPONENTWISE, SCORE_JOINT = 0, 1
 FP32, FP64 = 0, 1
 INPUTS_ON_DEVICE = 0x1
 ASYNC = 0x2
+R_UNIFORM = 0x4
 
 
 class EnsfParams(C.Structure):
@@ -186,13 +187,18 @@ def check(device: int, p: EnsfParams) -> Status:
 
 def analyze_host(members, y, r=1.0, idx=None, *, n_steps=100, eps=0.01, minibatch_j=0,
                  damping_t=1.0, relax_factor=1.0, seed=7, cycle=1, precision=FP32, device=-1,
-                 device_count=1, k0=0, d_total=None, arctan=False, joint=False):
+                 device_count=1, k0=0, d_total=None, arctan=False, joint=False,
+                 r_uniform=False):
     """numpy-in / numpy-out analysis over the window [k0, k0 + d) of a state
-    of dimension d_total (defaults to the whole state)."""
+    of dimension d_total (defaults to the whole state).  ``r_uniform``: pass
+    the scalar ``r`` once (TURBDA_R_UNIFORM) instead of an obs_dim copy."""
     x = np.ascontiguousarray(members, dtype=np.float64)
     m, d = x.shape
     y = np.ascontiguousarray(y, dtype=np.float64)
-    r = np.ascontiguousarray(np.broadcast_to(np.asarray(r, np.float64), y.shape))
+    if r_uniform:
+        r = np.array([float(r)], np.float64)
+    else:
+        r = np.ascontiguousarray(np.broadcast_to(np.asarray(r, np.float64), y.shape))
     ix = None if idx is None else np.ascontiguousarray(idx, dtype=np.int64)
     p = params(d_total=d if d_total is None else d_total, k0=k0, d_local=d, obs_dim=y.size,
                n_members=m, n_steps=n_steps, minibatch_j=minibatch_j,
@@ -200,7 +206,8 @@ def analyze_host(members, y, r=1.0, idx=None, *, n_steps=100, eps=0.01, minibatc
                damping_t=damping_t,
                relax_factor=relax_factor, seed=seed, cycle=cycle, precision=precision,
                device=device, device_count=device_count,
-               score_mode=SCORE_JOINT if joint else SCORE_COMPONENTWISE)
+               score_mode=SCORE_JOINT if joint else SCORE_COMPONENTWISE,
+               flags=R_UNIFORM if r_uniform else 0)
     out = np.empty_like(x)
     analyze(p, x, y, r, ix, out)
     return out

@@ -202,7 +202,8 @@ int validate(const turbda_ensf_params* p, turbda_status* st) {
 
 int validate_host_obs(const turbda_ensf_params* p, const double* r, const int64_t* idx,
                       turbda_status* st) {
-    for (int64_t q = 0; q < p->obs_dim; ++q)
+    const int64_t nr = (p->flags & TURBDA_R_UNIFORM) ? std::min<int64_t>(p->obs_dim, 1) : p->obs_dim;
+    for (int64_t q = 0; q < nr; ++q)
         if (!(r[q] > 0.0)) return fail(st, TURBDA_CONFIG, "observation: r_diag > 0");
     if (!obs_dense(p->obs_kind))
         for (int64_t q = 0; q < p->obs_dim; ++q)
@@ -291,7 +292,7 @@ struct Window {
     int64_t off() const { return k0_local; }
 };
 
-constexpr int kMaxChunks = 8;
+constexpr int kMaxChunks = 32;  // >= 8 MB each: the exposed first H2D and last D2H shrink
 
 int ws_streams(Workspace* w, int n, turbda_status* st) {
     while (int(w->cstreams.size()) < n) {
@@ -307,7 +308,7 @@ int ws_streams(Workspace* w, int n, turbda_status* st) {
 
 // Runs one analysis slice on one device.  Host mode: `forecast`/`out` are the
 // call's host arrays with row pitch p->d_local (or member rows); the slice
-// starts at column win.k0_local.  The slice is cut into up to kMaxChunks
+// starts at column win.k0_local.  The slice is cut into up to kMaxChunks (32)
 // contiguous coordinate chunks, each on its own stream, so the H2D copy of
 // chunk c+1, the kernels of chunk c and the D2H copy of chunk c-1 overlap
 // (chunks are independent: the score is componentwise).  Device mode:
@@ -317,6 +318,8 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
               const double* const* frows, const double* y, const double* r, const int64_t* idx,
               double* out, double* const* orows, cudaStream_t user_stream, turbda_status* st) {
     const bool on_dev = (p->flags & TURBDA_INPUTS_ON_DEVICE) != 0;
+    const bool r_uni = (p->flags & TURBDA_R_UNIFORM) != 0;
+    const int64_t r_stride = r_uni ? 0 : 1;
     TB_CUDA(cudaSetDevice(device));
     Workspace* w = workspace(device);
     std::lock_guard<std::mutex> lk(w->mu);
@@ -383,6 +386,8 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
         TB_CUDA(w->r.reserve(sizeof(double) * nb));
         dy = w->y.as<double>();
         dr = w->r.as<double>();
+        if (r_uni && p->obs_dim > 0)
+            TB_CUDA(cudaMemcpyAsync(w->r.p, r, sizeof(double), cudaMemcpyHostToDevice, s));
         if (!obs_dense(p->obs_kind)) {
             // selection entries are global: every chunk scans all of them
             TB_CUDA(w->idx.reserve(sizeof(int64_t) * nb));
@@ -390,8 +395,9 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
             if (p->obs_dim > 0) {
                 TB_CUDA(cudaMemcpyAsync(w->y.p, y, sizeof(double) * size_t(p->obs_dim),
                                         cudaMemcpyHostToDevice, s));
-                TB_CUDA(cudaMemcpyAsync(w->r.p, r, sizeof(double) * size_t(p->obs_dim),
-                                        cudaMemcpyHostToDevice, s));
+                if (!r_uni)
+                    TB_CUDA(cudaMemcpyAsync(w->r.p, r, sizeof(double) * size_t(p->obs_dim),
+                                            cudaMemcpyHostToDevice, s));
                 TB_CUDA(cudaMemcpyAsync(w->idx.p, idx, sizeof(int64_t) * size_t(p->obs_dim),
                                         cudaMemcpyHostToDevice, s));
             }
@@ -444,17 +450,19 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
             if (obs_dense(p->obs_kind) && c.dl > 0) {
                 TB_CUDA(cudaMemcpyAsync(w->y.as<double>() + c.k0_local, y + col,
                                         sizeof(double) * size_t(c.dl), cudaMemcpyHostToDevice, cs));
-                TB_CUDA(cudaMemcpyAsync(w->r.as<double>() + c.k0_local, r + col,
-                                        sizeof(double) * size_t(c.dl), cudaMemcpyHostToDevice, cs));
+                if (!r_uni)
+                    TB_CUDA(cudaMemcpyAsync(w->r.as<double>() + c.k0_local, r + col,
+                                            sizeof(double) * size_t(c.dl), cudaMemcpyHostToDevice,
+                                            cs));
             }
         }
         const int64_t k0c = p->k0 + col;
         double2* abc = w->ab.as<double2>() + c.k0_local;
         const bool dense = obs_dense(p->obs_kind);
         const double* yc = dense ? dy + c.k0_local : dy;
-        const double* rc_ = dense ? dr + c.k0_local : dr;
+        const double* rc_ = (dense && !r_uni) ? dr + c.k0_local : dr;
         const int64_t nobs = dense ? c.dl : p->obs_dim;
-        TB_CUDA(launch_obs_prep(yc, rc_, didx, nobs, p->obs_kind, k0c, c.dl, abc, cs));
+        TB_CUDA(launch_obs_prep(yc, rc_, didx, nobs, p->obs_kind, k0c, c.dl, abc, cs, r_stride));
         ++g_launches;
         a.k0 = k0c;
         a.dl = c.dl;
@@ -584,6 +592,7 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
               double* out, double* const* orows, cudaStream_t user_stream, void* comm,
               turbda_status* st) {
     const bool on_dev = (p->flags & TURBDA_INPUTS_ON_DEVICE) != 0;
+    const bool r_uni = (p->flags & TURBDA_R_UNIFORM) != 0;
     TB_CUDA(cudaSetDevice(device));
     Workspace* w = workspace(device);
     std::lock_guard<std::mutex> lk(w->mu);
@@ -621,7 +630,8 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
         if (nobs > 0) {
             TB_CUDA(cudaMemcpyAsync(w->y.p, dense ? y + win.k0_local : y, sizeof(double) * size_t(nobs),
                                     cudaMemcpyHostToDevice, s));
-            TB_CUDA(cudaMemcpyAsync(w->r.p, dense ? r + win.k0_local : r, sizeof(double) * size_t(nobs),
+            TB_CUDA(cudaMemcpyAsync(w->r.p, (dense && !r_uni) ? r + win.k0_local : r,
+                                    sizeof(double) * size_t(r_uni ? 1 : nobs),
                                     cudaMemcpyHostToDevice, s));
             if (!dense)
                 TB_CUDA(cudaMemcpyAsync(w->idx.p, idx, sizeof(int64_t) * size_t(nobs),
@@ -644,8 +654,8 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
     TB_CUDA(cudaMemsetAsync(dstatus, 0xff, sizeof(unsigned long long), s));
 
     const int64_t k0g = p->k0 + win.k0_local;
-    TB_CUDA(launch_obs_prep(dense ? dy : dy, dr, didx, dense ? dl : p->obs_dim, p->obs_kind, k0g,
-                            dl, w->ab.as<double2>(), s));
+    TB_CUDA(launch_obs_prep(dy, dr, didx, dense ? dl : p->obs_dim, p->obs_kind, k0g, dl,
+                            w->ab.as<double2>(), s, r_uni ? 0 : 1));
     KernelArgs a{};
     a.d_total = p->d_total;
     a.k0 = k0g;

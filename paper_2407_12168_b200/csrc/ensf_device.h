@@ -55,7 +55,7 @@ constexpr unsigned long long kNoDivergence = ~0ull;
 // obs (y, r, idx) -> per-coordinate {A = sum 1/r, B = sum y/r} over the window
 cudaError_t launch_obs_prep(const double* y, const double* r, const int64_t* idx,
                             int64_t obs_dim, int obs_kind, int64_t k0, int64_t dl,
-                            double2* ab, cudaStream_t st);
+                            double2* ab, cudaStream_t st, int64_t r_stride = 1);
 
 // full fused analysis into z (fp32 or fp64 scratch, [m][dl]).  The fp32 path
 // first converts (and, without minibatches, sorts per coordinate) the

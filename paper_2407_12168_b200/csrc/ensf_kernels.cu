@@ -535,23 +535,25 @@ __global__ void relax_kernel(const T* __restrict__ z, const double* __restrict__
 // obs -> per-coordinate {A, B}.  Identity: one entry per coordinate.
 // Selection: entries whose global index falls in the window are scattered
 // (duplicate indices add, as adjoint_scatter does, proj/src/observation.cpp:18-27).
+// r_stride 0: one error variance for every observation (TURBDA_R_UNIFORM)
 __global__ void obs_identity_kernel(const double* __restrict__ y, const double* __restrict__ r,
-                                    int64_t dl, double2* __restrict__ ab) {
+                                    int64_t r_stride, int64_t dl, double2* __restrict__ ab) {
     const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k < dl) {
-        const double inv = 1.0 / r[k];
+        const double inv = 1.0 / r[k * r_stride];
         ab[k] = make_double2(inv, y[k] * inv);
     }
 }
 
 __global__ void obs_select_kernel(const double* __restrict__ y, const double* __restrict__ r,
-                                  const int64_t* __restrict__ idx, int64_t obs_dim, int64_t k0,
-                                  int64_t dl, double2* __restrict__ ab) {
+                                  int64_t r_stride, const int64_t* __restrict__ idx,
+                                  int64_t obs_dim, int64_t k0, int64_t dl,
+                                  double2* __restrict__ ab) {
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= obs_dim) return;
     const int64_t k = idx[q] - k0;
     if (k < 0 || k >= dl) return;
-    const double inv = 1.0 / r[q];
+    const double inv = 1.0 / r[q * r_stride];
     atomicAdd(&ab[k].x, inv);
     atomicAdd(&ab[k].y, y[q] * inv);
 }
@@ -688,15 +690,16 @@ cudaError_t launch_f64_p(const KernelArgs& a, const double* x, const double2* ab
 
 cudaError_t launch_obs_prep(const double* y, const double* r, const int64_t* idx,
                             int64_t obs_dim, int obs_kind, int64_t k0, int64_t dl, double2* ab,
-                            cudaStream_t st) {
+                            cudaStream_t st, int64_t r_stride) {
     if (dl <= 0) return cudaSuccess;
     if (obs_dense(obs_kind)) {
-        obs_identity_kernel<<<blocks_for(dl, 256), 256, 0, st>>>(y, r, dl, ab);
+        obs_identity_kernel<<<blocks_for(dl, 256), 256, 0, st>>>(y, r, r_stride, dl, ab);
         return cudaGetLastError();
     }
     cudaError_t e = cudaMemsetAsync(ab, 0, sizeof(double2) * size_t(dl), st);
     if (e != cudaSuccess || obs_dim == 0) return e;
-    obs_select_kernel<<<blocks_for(obs_dim, 256), 256, 0, st>>>(y, r, idx, obs_dim, k0, dl, ab);
+    obs_select_kernel<<<blocks_for(obs_dim, 256), 256, 0, st>>>(y, r, r_stride, idx, obs_dim, k0,
+                                                                   dl, ab);
     return cudaGetLastError();
 }
 

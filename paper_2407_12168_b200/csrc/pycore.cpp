@@ -58,7 +58,6 @@ py::array_t<double> ensf_analyze(const darray& members, const turbda::GridSpec& 
     if (y.size() != obs_dim) throw turbda::DimensionError("observation: length mismatch");
     if (!(r > 0.0)) throw turbda::ConfigError("observation: r_diag > 0");
     if (state_dim != d) throw turbda::DimensionError("analyze: observation operator dimension");
-    const std::vector<double> rr(size_t(obs_dim), r);
 
     turbda_ensf_params p;
     turbda_ensf_params_init(&p);
@@ -82,6 +81,7 @@ py::array_t<double> ensf_analyze(const darray& members, const turbda::GridSpec& 
     p.precision = parse_precision(precision);
     p.device = device;
     p.device_count = device_count;
+    p.flags = TURBDA_R_UNIFORM;  // the scalar r, not an obs_dim-long copy of it
 
     // out=: a caller-owned (M, d) float64 C-contiguous array (e.g. pinned
     // host memory) receives the analysis; otherwise a new array is returned
@@ -98,7 +98,7 @@ py::array_t<double> ensf_analyze(const darray& members, const turbda::GridSpec& 
     int rc;
     {
         py::gil_scoped_release nogil;
-        rc = turbda_ensf_analyze(&p, members.data(), y.data(), rr.data(),
+        rc = turbda_ensf_analyze(&p, members.data(), y.data(), &r,
                                  idx.empty() ? nullptr : idx.data(), out.mutable_data(), nullptr,
                                  &st);
     }

@@ -77,6 +77,17 @@ def test_r_must_be_positive_host_mode():
     assert ei.value.code == capi.CONFIG and b"r_diag" in bytes(ei.value.args[0], "utf8")
 
 
+def test_uniform_r_validated_before_device():
+    """TURBDA_R_UNIFORM: the one r value is checked (r > 0) before any device
+    work; the other obs_dim - 1 entries are never read."""
+    from paper_2407_12168_b200 import capi
+    x = np.zeros((4, 8))
+    p = capi.params(d_total=8, d_local=8, obs_dim=8, n_members=4, flags=capi.R_UNIFORM)
+    with pytest.raises(capi.TurbdaError) as ei:
+        capi.analyze(p, x, np.zeros(8), np.array([-1.0]), None, np.zeros_like(x))
+    assert ei.value.code == capi.CONFIG
+
+
 def test_python_module_mirrors_reference_binding():
     import paper_2407_12168_b200 as tb
     assert issubclass(tb.ConfigError, ValueError) and issubclass(tb.DimensionError, ValueError)

@@ -196,6 +196,35 @@ def test_device_pointer_path_matches_host_path(capi):
     assert np.array_equal(out.cpu().numpy(), host)
 
 
+@pytest.mark.parametrize("precision,stride,joint", [(0, 1, False), (0, 4, False), (1, 4, False),
+                                                    (1, 1, True)])
+def test_uniform_r_flag_matches_r_array(capi, precision, stride, joint):
+    """TURBDA_R_UNIFORM (one r for every observation) == the obs_dim-long r
+    array, bit for bit, through host buffers, device-count splits and device
+    pointers."""
+    torch = pytest.importorskip("torch")
+    x, y, idx = throughput_inputs(20, 3000, stride=stride)
+    kw = dict(n_steps=40, precision=precision, joint=joint)
+    full = capi.analyze_host(x, y, 0.6, idx, **kw)
+    assert np.array_equal(capi.analyze_host(x, y, 0.6, idx, r_uniform=True, **kw), full)
+    if capi.device_count() > 1 and not joint:
+        split = capi.analyze_host(x, y, 0.6, idx, r_uniform=True, device=0, device_count=2, **kw)
+        assert np.array_equal(split, full)
+    dev = torch.device("cuda:0")
+    tx = torch.from_numpy(x).to(dev)
+    ty = torch.from_numpy(y).to(dev)
+    tr = torch.tensor([0.6], dtype=torch.float64, device=dev)
+    ti = None if idx is None else torch.from_numpy(idx).to(dev)
+    out = torch.empty_like(tx)
+    p = capi.params(d_total=3000, d_local=3000, obs_dim=y.size, n_members=20, n_steps=40,
+                    obs_kind=0 if idx is None else 1, precision=precision, device=0,
+                    score_mode=capi.SCORE_JOINT if joint else capi.SCORE_COMPONENTWISE,
+                    flags=capi.INPUTS_ON_DEVICE | capi.R_UNIFORM)
+    capi.analyze(p, tx, ty, tr, ti, out, stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), full)
+
+
 @pytest.mark.slow
 def test_cfg2_full_size_properties(capi):
     """BASELINE config 2 at full size (d=131072, N=64, S=100, stride-4 obs):
