@@ -18,6 +18,11 @@
  *                                                    src/ensf.cpp:68-82,96-106
  *   turbda_diag           <- turbda::rmse / spread    include/turbda/ensemble.hpp:32-38,
  *                                                    src/ensemble.cpp:18-43
+ *   turbda_letkf_analyze  <- turbda::letkf_analyze    include/turbda/letkf.hpp:48-52,
+ *                                                    src/letkf.cpp:57-175
+ *   turbda_rtps_inflate   <- turbda::rtps_inflate     include/turbda/letkf.hpp:54-56,
+ *                                                    src/letkf.cpp:177-207
+ *   turbda_gaspari_cohn   <- turbda::gaspari_cohn     src/letkf.cpp:10-18
  *
  * Error convention: every entry point returns a turbda_code and fills
  * *status (when non-NULL).  The C++ host maps TURBDA_CONFIG -> ConfigError,
@@ -54,7 +59,9 @@ typedef enum turbda_code {
     TURBDA_CUDA = 5,       /* no device / CUDA runtime failure             */
     TURBDA_INTERNAL = 6,
     TURBDA_BLOWUP = 7,     /* BlowupError(time, member): SQG state non-finite */
-    TURBDA_ABORTED = 8     /* RunAbortedError(cycle): status.diverged_step  */
+    TURBDA_ABORTED = 8,    /* RunAbortedError(cycle): status.diverged_step  */
+    TURBDA_SINGULAR = 9    /* SingularAnalysisError(ix, iy): LETKF, grid point */
+                           /* in status.diverged_particle / diverged_step    */
 } turbda_code;
 
 typedef enum turbda_precision {
@@ -255,6 +262,41 @@ TURBDA_API void turbda_experiment_init(turbda_experiment* e);
 TURBDA_API int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* records,
                           int32_t max_records, int32_t* n_records, double* max_cfl,
                           double* phase_seconds, turbda_status* status);
+
+/* -------------------------------------------------------------------------
+ * LETKF arm: letkf_analyze / rtps_inflate /
+ * gaspari_cohn, proj/include/turbda/letkf.hpp:11-56, proj/src/letkf.cpp:10-207.
+ * Grid operators only (identity / index selection, optional arctan), the
+ * observations located on the grid (operator_locations,
+ * proj/src/observation.cpp:43-60) unless `locations` ([obs_dim][2]) is given.
+ * fp64; agrees with the reference formulation to rounding.
+ * ------------------------------------------------------------------------- */
+typedef struct turbda_letkf_params { /* LetkfConfig + GridSpec + Observation shape */
+    int32_t nx, ny;         /* grid (nz = 2), nx == ny (isotropic metric)        */
+    int32_t n_members;      /* M                                                 */
+    int32_t obs_kind;       /* as turbda_ensf_params.obs_kind                    */
+    int64_t obs_dim;
+    double cutoff_km;       /* LetkfConfig::cutoff_km (default 2000)             */
+    double domain_km;       /* LetkfConfig::domain_km (default 20000)            */
+    double rtps_alpha;      /* LetkfConfig::rtps_alpha in [0, 1] (default 0.3)   */
+    int32_t device;         /* -1 = current device                               */
+    uint32_t flags;         /* TURBDA_INPUTS_ON_DEVICE | TURBDA_R_UNIFORM        */
+} turbda_letkf_params;
+
+TURBDA_API void turbda_letkf_params_init(turbda_letkf_params* p);
+/* forecast / analysis_out: [M][2 nx ny] fp64; y, r_diag [obs_dim];
+ * obs_idx [obs_dim] for kinds 1/3; locations optional.  TURBDA_SINGULAR when a
+ * local transform has a non-positive eigenvalue. */
+TURBDA_API int turbda_letkf_analyze(const turbda_letkf_params* p, const double* forecast,
+                                    const double* y, const double* r_diag,
+                                    const int64_t* obs_idx, const double* locations,
+                                    double* analysis_out, void* stream, turbda_status* status);
+/* RTPS inflation of an [M][d] analysis towards the background spread */
+TURBDA_API int turbda_rtps_inflate(const double* analysis, const double* background, int32_t m,
+                                   int64_t d, double alpha, double* out, int32_t device,
+                                   uint32_t flags, void* stream, turbda_status* status);
+/* Gaspari-Cohn correlation at normalized distance r (TURBDA_CONFIG for r < 0) */
+TURBDA_API int turbda_gaspari_cohn(double r, double* out, turbda_status* status);
 
 /* Number of CUDA devices (0 when none), library ABI version, and the name of
  * the kernel family compiled in ("sm_100a"). */

@@ -16,8 +16,8 @@ import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libturbda_b200.so"
 
-OK, CONFIG, DIMENSION, DIVERGED, DOMAIN, CUDA, INTERNAL, BLOWUP, ABORTED = range(9)
-VARIANT_FREE_RUN, VARIANT_ENSF = 0, 2
+OK, CONFIG, DIMENSION, DIVERGED, DOMAIN, CUDA, INTERNAL, BLOWUP, ABORTED, SINGULAR = range(10)
+VARIANT_FREE_RUN, VARIANT_LETKF, VARIANT_ENSF = 0, 1, 2
 SCORE_COMPONENTWISE, SCORE_JOINT = 0, 1
 FP32, FP64 = 0, 1
 INPUTS_ON_DEVICE = 0x1
@@ -55,6 +55,13 @@ class Experiment(C.Structure):
                 ("me_enabled", C.c_int32), ("me_ncomp", C.c_int32),
                 ("me_base_amplitude", C.c_double), ("me_prob", C.c_double * 8),
                 ("me_frac", C.c_double * 8)]
+
+
+class LetkfParams(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("n_members", C.c_int32),
+                ("obs_kind", C.c_int32), ("obs_dim", C.c_int64), ("cutoff_km", C.c_double),
+                ("domain_km", C.c_double), ("rtps_alpha", C.c_double), ("device", C.c_int32),
+                ("flags", C.c_uint32)]
 
 
 class Status(C.Structure):
@@ -136,6 +143,16 @@ def lib() -> C.CDLL:
         L.turbda_run_experiment.argtypes = [C.POINTER(Experiment), C.c_int32, vp, C.c_int32,
                                             C.POINTER(C.c_int32), dp, vp, C.POINTER(Status)]
         L.turbda_run_experiment.restype = C.c_int
+        L.turbda_letkf_params_init.argtypes = [C.POINTER(LetkfParams)]
+        L.turbda_letkf_params_init.restype = None
+        L.turbda_letkf_analyze.argtypes = [C.POINTER(LetkfParams), vp, vp, vp, vp, vp, vp, vp,
+                                           C.POINTER(Status)]
+        L.turbda_letkf_analyze.restype = C.c_int
+        L.turbda_rtps_inflate.argtypes = [vp, vp, C.c_int32, C.c_int64, C.c_double, vp,
+                                          C.c_int32, C.c_uint32, vp, C.POINTER(Status)]
+        L.turbda_rtps_inflate.restype = C.c_int
+        L.turbda_gaspari_cohn.argtypes = [C.c_double, dp, C.POINTER(Status)]
+        L.turbda_gaspari_cohn.restype = C.c_int
         _lib = L
     return _lib
 
@@ -211,6 +228,72 @@ def analyze_host(members, y, r=1.0, idx=None, *, n_steps=100, eps=0.01, minibatc
     out = np.empty_like(x)
     analyze(p, x, y, r, ix, out)
     return out
+
+
+def letkf_params(**kw) -> LetkfParams:
+    p = LetkfParams()
+    lib().turbda_letkf_params_init(C.byref(p))
+    for k, v in kw.items():
+        if not hasattr(p, k):
+            raise TypeError(f"unknown turbda_letkf_params field {k!r}")
+        setattr(p, k, v)
+    return p
+
+
+def letkf_raw(p: LetkfParams, forecast, y, r_diag, obs_idx, locations, out,
+              stream: int | None = None):
+    """Raw C-ABI call (host numpy arrays, or device buffers with
+    ``p.flags & INPUTS_ON_DEVICE``)."""
+    st = Status()
+    code = lib().turbda_letkf_analyze(C.byref(p), _ptr(forecast), _ptr(y), _ptr(r_diag),
+                                      _ptr(obs_idx), _ptr(locations), _ptr(out), stream,
+                                      C.byref(st))
+    _check(code, st)
+
+
+def letkf_analyze(members, y, r=1.0, idx=None, *, nx, ny, cutoff_km=2000.0, domain_km=20000.0,
+                  rtps_alpha=0.3, arctan=False, locations=None, device=-1, r_uniform=False):
+    """numpy-in / numpy-out LETKF analysis of an (M, 2*nx*ny) ensemble."""
+    x = np.ascontiguousarray(members, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if r_uniform:
+        rr = np.array([float(r)], np.float64)
+    else:
+        rr = np.ascontiguousarray(np.broadcast_to(np.asarray(r, np.float64), y.shape))
+    ix = None if idx is None else np.ascontiguousarray(idx, dtype=np.int64)
+    loc = None if locations is None else np.ascontiguousarray(locations, dtype=np.float64)
+    p = letkf_params(nx=nx, ny=ny, n_members=x.shape[0],
+                     obs_kind=(0 if idx is None else 1) + (2 if arctan else 0), obs_dim=y.size,
+                     cutoff_km=cutoff_km, domain_km=domain_km, rtps_alpha=rtps_alpha,
+                     device=device, flags=R_UNIFORM if r_uniform else 0)
+    if x.shape[1] != 2 * nx * ny:
+        raise TurbdaError(DIMENSION, _status_msg("letkf_analyze: state/grid size mismatch"))
+    out = np.empty_like(x)
+    letkf_raw(p, x, y, rr, ix, loc, out)
+    return out
+
+
+def rtps_inflate(analysis, background, alpha, device=-1):
+    a = np.ascontiguousarray(analysis, np.float64)
+    b = np.ascontiguousarray(background, np.float64)
+    out = np.empty_like(a)
+    st = Status()
+    _check(lib().turbda_rtps_inflate(_ptr(a), _ptr(b), a.shape[0], a.shape[1], alpha, _ptr(out),
+                                     device, 0, None, C.byref(st)), st)
+    return out
+
+
+def gaspari_cohn(r: float) -> float:
+    v = C.c_double()
+    st = Status()
+    _check(lib().turbda_gaspari_cohn(r, C.byref(v), C.byref(st)), st)
+    return v.value
+
+
+def _status_msg(msg: str) -> Status:
+    st = Status()
+    st.msg = msg.encode()[:255]
+    return st
 
 
 def score(z, t, members, batch=None, eps=0.01, y=None, r=None, idx=None, damping_t=1.0,

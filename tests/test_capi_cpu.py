@@ -114,3 +114,35 @@ def test_no_cpu_fallback_without_device():
     with pytest.raises(capi.TurbdaError) as ei:
         capi.analyze(p, x, np.zeros(8), np.ones(8), None, np.zeros_like(x))
     assert ei.value.code == capi.CUDA
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(nx=8, ny=16), "CONFIG"),            # isotropic metric, proj/src/letkf.cpp:62-63
+    (dict(rtps_alpha=1.5), "CONFIG"),         # LetkfConfig::validate
+    (dict(cutoff_km=0.0), "CONFIG"),
+    (dict(nx=6, ny=6), "CONFIG"),             # GridSpec::validate
+    (dict(obs_dim=100), "DIMENSION"),         # identity operator of the wrong size
+])
+def test_letkf_validation_before_device(kw, code):
+    """LETKF arm: argument checks precede any device work,
+    as the reference's letkf input-validation test expects
+    (proj/tests/test_letkf.cpp:310-337)."""
+    from paper_2407_12168_b200 import capi
+    base = dict(nx=8, ny=8, n_members=4, obs_kind=0, obs_dim=128)
+    base.update(kw)
+    p = capi.letkf_params(**base)
+    x = np.zeros((4, 2 * p.nx * p.ny))
+    with pytest.raises(capi.TurbdaError) as ei:
+        capi.letkf_raw(p, x, np.zeros(p.obs_dim), np.ones(p.obs_dim), None, None,
+                       np.zeros_like(x))
+    assert ei.value.code == getattr(capi, code)
+
+
+def test_gaspari_cohn_host_entry():
+    from paper_2407_12168_b200 import capi
+    assert capi.gaspari_cohn(0.0) == 1.0
+    assert capi.gaspari_cohn(1.0) == pytest.approx(5.0 / 24.0, rel=1e-14)
+    assert capi.gaspari_cohn(1.5) == pytest.approx(19.0 / 1152.0, rel=1e-13)
+    assert capi.gaspari_cohn(2.0) == 0.0
+    with pytest.raises(capi.TurbdaError):
+        capi.gaspari_cohn(-0.1)
