@@ -232,7 +232,8 @@ TURBDA_API int turbda_nature_run(const turbda_sqg_params* p, double spinup, doub
                       int32_t* n_snaps, int32_t device, turbda_status* status);
 
 #define TURBDA_VARIANT_FREE_RUN 0
-#define TURBDA_VARIANT_ENSF 2 /* (1 = letkf is not part of this build) */
+#define TURBDA_VARIANT_LETKF 1 /* turbda_letkf_analyze on the device each cycle */
+#define TURBDA_VARIANT_ENSF 2
 
 typedef struct turbda_experiment { /* ExperimentConfig, proj/include/turbda/osse.hpp:30-50 */
     turbda_sqg_params sqg;
@@ -249,6 +250,8 @@ typedef struct turbda_experiment { /* ExperimentConfig, proj/include/turbda/osse
     int32_t me_enabled, me_ncomp;  /* ModelErrorConfig                          */
     double me_base_amplitude;      /* <= 0: climatological RMS of the nature run */
     double me_prob[8], me_frac[8];
+    double letkf_cutoff_km, letkf_domain_km, letkf_rtps_alpha; /* LetkfConfig */
+    int32_t letkf_obs_thinning, reserved;
 } turbda_experiment;
 
 TURBDA_API void turbda_experiment_init(turbda_experiment* e);

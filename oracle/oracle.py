@@ -354,7 +354,8 @@ def conditioned_inputs(m, d, oracle=None, stride=0):
 class RefCycleOracle:
     """The reference's cycle driver and SQG model (proj/src/{osse,config,
     forecast,sqg,spectral}.cpp + the hot path), unmodified, built against
-    cuFFTW (oracle/ref_cycle_shim.cpp).  Needs a GPU at run time."""
+    cuFFTW (oracle/ref_cycle_shim.cpp).  Needs a GPU at run time, except
+    ``letkf_analyze`` (the Eigen-free LETKF restatement, CPU only)."""
 
     kind = "reference"
 
@@ -372,6 +373,27 @@ class RefCycleOracle:
         L.refc_nature_run.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                       C.c_double, C.c_double, C.c_double, C.c_uint64, _dp,
                                       C.c_int, C.POINTER(C.c_int), C.c_char_p, C.c_int]
+        L.refc_letkf_analyze.restype = C.c_int
+        L.refc_letkf_analyze.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp, _dp, C.c_void_p,
+                                         C.c_int64, C.c_double, C.c_double, C.c_double, C.c_int,
+                                         _dp, C.c_char_p, C.c_int]
+
+    def letkf_analyze(self, x, y, r, idx, nx, ny, cutoff_km=2000.0, domain_km=20000.0,
+                      rtps_alpha=0.3, workers=0):
+        """The C++ LETKF restatement (oracle/letkf_restated.cpp) through the
+        reference's own Ensemble / Observation types; CPU only."""
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.ascontiguousarray(y, np.float64)
+        r = np.ascontiguousarray(np.broadcast_to(np.asarray(r, np.float64), y.shape))
+        ix = None if idx is None else np.ascontiguousarray(idx, np.int64)
+        out = np.empty_like(x)
+        msg = C.create_string_buffer(512)
+        code = self.lib.refc_letkf_analyze(
+            x, x.shape[0], nx, ny, y, r, None if ix is None else ix.ctypes.data, y.size,
+            cutoff_km, domain_km, rtps_alpha, workers, out, msg, 512)
+        if code:
+            raise OracleError(5, msg.value.decode())
+        return out
 
     def run_experiment(self, config: dict, workers=0):
         import json

@@ -6,6 +6,9 @@
 //                          (JSON config: turbda::config_from_json, proj/src/config.cpp:64-131)
 //   refc_sqg_advance    -> turbda::SqgStepper::advance proj/src/forecast.cpp:14-32
 //   refc_nature_run     -> turbda::nature_run      proj/src/osse.cpp:101-135
+//   refc_letkf_analyze  -> turbda::letkf_analyze   (restated without Eigen,
+//                          oracle/letkf_restated.cpp; the cycle driver's
+//                          "letkf" variant calls the same function)
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -18,12 +21,6 @@
 #include "turbda/forecast.hpp"
 #include "turbda/osse.hpp"
 
-namespace turbda {
-Ensemble letkf_analyze(const Ensemble&, const Observation&, const LetkfConfig&, const GridSpec&,
-                       int) {
-    throw ConfigError("letkf is not built in the cycle oracle");
-}
-}  // namespace turbda
 
 using namespace turbda;
 
@@ -105,6 +102,48 @@ int refc_nature_run(int nx, int ny, double lx, double ly, double h, double spinu
             ++n;
         }
         *n_snaps = n;
+        return 0;
+    } catch (const std::exception& e) {
+        put(msg, msglen, e.what());
+        return 1;
+    }
+}
+
+// forecast / out: [m][2 nx ny]; idx == nullptr: identity operator
+int refc_letkf_analyze(const double* forecast, int m, int nx, int ny, const double* y,
+                       const double* r, const int64_t* idx, int64_t nobs, double cutoff_km,
+                       double domain_km, double rtps_alpha, int workers, double* out, char* msg,
+                       int msglen) {
+    try {
+        GridSpec g;
+        g.nx = nx;
+        g.ny = ny;
+        g.lx = g.ly = 62.83185307179586 * (nx / 64.0);
+        const size_t d = g.grid_size();
+        Ensemble ens;
+        ens.valid_time = 0.0;
+        for (int j = 0; j < m; ++j) {
+            ens.members.emplace_back(forecast + size_t(j) * d, forecast + size_t(j + 1) * d);
+            ens.member_seeds.push_back(uint64_t(j) + 1);
+        }
+        Observation obs;
+        if (idx) {
+            obs.op = ObsOperator{ObsOperatorKind::index_selection, d,
+                                 std::vector<std::size_t>(idx, idx + nobs)};
+        } else {
+            obs.op = ObsOperator{ObsOperatorKind::identity, d, {}};
+        }
+        obs.locations = operator_locations(g, obs.op);
+        obs.y.assign(y, y + nobs);
+        obs.r_diag.assign(r, r + nobs);
+        obs.time = 0.0;
+        LetkfConfig cfg;
+        cfg.cutoff_km = cutoff_km;
+        cfg.domain_km = domain_km;
+        cfg.rtps_alpha = rtps_alpha;
+        const Ensemble an = letkf_analyze(ens, obs, cfg, g, workers);
+        for (int j = 0; j < m; ++j)
+            std::memcpy(out + size_t(j) * d, an.members[size_t(j)].data(), sizeof(double) * d);
         return 0;
     } catch (const std::exception& e) {
         put(msg, msglen, e.what());

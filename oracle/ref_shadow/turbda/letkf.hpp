@@ -1,8 +1,8 @@
 // TEST INFRASTRUCTURE ONLY - stand-in for proj/include/turbda/letkf.hpp so
 // the reference's cycle driver (proj/src/osse.cpp, proj/src/config.cpp)
 // compiles without Eigen.  LetkfConfig matches the reference
-// (proj/include/turbda/letkf.hpp:12-27); letkf_analyze is never reached by
-// the EnSF experiments run here (it throws if it is).
+// (proj/include/turbda/letkf.hpp:12-27); letkf_analyze / rtps_inflate /
+// gaspari_cohn are the Eigen-free restatement in oracle/letkf_restated.cpp.
 #pragma once
 #include <cstdint>
 
@@ -27,7 +27,9 @@ struct LetkfConfig {
     }
 };
 
+double gaspari_cohn(double r);
 Ensemble letkf_analyze(const Ensemble& forecast, const Observation& obs,
                        const LetkfConfig& cfg, const GridSpec& grid, int workers = 0);
+Ensemble rtps_inflate(const Ensemble& analysis, const Ensemble& background, double alpha);
 
 }  // namespace turbda

@@ -54,7 +54,9 @@ class Experiment(C.Structure):
                 ("relax_factor", C.c_double), ("precision", C.c_int32), ("score_mode", C.c_int32),
                 ("me_enabled", C.c_int32), ("me_ncomp", C.c_int32),
                 ("me_base_amplitude", C.c_double), ("me_prob", C.c_double * 8),
-                ("me_frac", C.c_double * 8)]
+                ("me_frac", C.c_double * 8), ("letkf_cutoff_km", C.c_double),
+                ("letkf_domain_km", C.c_double), ("letkf_rtps_alpha", C.c_double),
+                ("letkf_obs_thinning", C.c_int32), ("reserved", C.c_int32)]
 
 
 class LetkfParams(C.Structure):

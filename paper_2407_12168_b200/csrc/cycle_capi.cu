@@ -376,6 +376,11 @@ void turbda_experiment_init(turbda_experiment* e) {
         e->me_prob[c] = prob[c];
         e->me_frac[c] = frac[c];
     }
+    // LetkfConfig defaults, proj/include/turbda/letkf.hpp:13-16
+    e->letkf_cutoff_km = 2000.0;
+    e->letkf_domain_km = 20000.0;
+    e->letkf_rtps_alpha = 0.3;
+    e->letkf_obs_thinning = 0;
 }
 
 int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* records,
@@ -387,8 +392,15 @@ int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* re
         for (int q = 0; q < 4; ++q) phase_seconds[q] = 0.0;
     // ExperimentConfig::validate, proj/src/osse.cpp:40-62
     if (int rc = validate_sqg(&e->sqg, st)) return rc;
-    if (e->variant != TURBDA_VARIANT_ENSF && e->variant != TURBDA_VARIANT_FREE_RUN)
-        return fail(st, TURBDA_CONFIG, "run_experiment: only the free_run and ensf variants exist here");
+    if (e->variant != TURBDA_VARIANT_ENSF && e->variant != TURBDA_VARIANT_FREE_RUN &&
+        e->variant != TURBDA_VARIANT_LETKF)
+        return fail(st, TURBDA_CONFIG, "run_experiment: unknown variant");
+    // LetkfConfig::validate (called for every variant, proj/src/osse.cpp:43)
+    if (!(e->letkf_cutoff_km > 0.0) || !(e->letkf_domain_km > 0.0))
+        return fail(st, TURBDA_CONFIG, "letkf: cutoff_km, domain_km > 0");
+    if (!(e->letkf_rtps_alpha >= 0.0 && e->letkf_rtps_alpha <= 1.0))
+        return fail(st, TURBDA_CONFIG, "letkf: rtps_alpha in [0, 1]");
+    if (e->letkf_obs_thinning < 0) return fail(st, TURBDA_CONFIG, "letkf: obs_thinning >= 0");
     if (!(e->eps > 0.0 && e->eps < 1.0)) return fail(st, TURBDA_CONFIG, "ensf: eps must lie in (0, 1)");
     if (e->n_steps < 10) return fail(st, TURBDA_CONFIG, "ensf: n_steps >= 10");
     if (e->minibatch_j < 0) return fail(st, TURBDA_CONFIG, "ensf: minibatch_j >= 0");
@@ -546,6 +558,19 @@ int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* re
     ap.flags = TURBDA_INPUTS_ON_DEVICE;
     ap.score_mode = e->score_mode;
 
+    turbda_letkf_params lp;
+    turbda_letkf_params_init(&lp);
+    lp.nx = cfg.nx;
+    lp.ny = cfg.ny;
+    lp.n_members = m;
+    lp.obs_kind = ap.obs_kind;
+    lp.obs_dim = nobs;
+    lp.cutoff_km = e->letkf_cutoff_km;
+    lp.domain_km = e->letkf_domain_km;
+    lp.rtps_alpha = e->letkf_rtps_alpha;
+    lp.device = dev;
+    lp.flags = TURBDA_INPUTS_ON_DEVICE;
+
     const auto metrics = [&](const double* x, const double* tr, double* rmse_out,
                              double* spread_out) -> int {
         if (cudaError_t ce = launch_diag(x, m, d, tr, ddiag.as<double>(), s); ce != cudaSuccess)
@@ -597,8 +622,12 @@ int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* re
             CY_CUDA(cudaGetLastError());
             ap.cycle = uint64_t(k);
             turbda_status ast{};
-            const int rc = turbda_ensf_analyze(&ap, ens.as<double>(), dy.as<double>(), dr.as<double>(),
-                                               didx.as<int64_t>(), ens_out.as<double>(), s, &ast);
+            const int rc =
+                e->variant == TURBDA_VARIANT_LETKF
+                    ? turbda_letkf_analyze(&lp, ens.as<double>(), dy.as<double>(), dr.as<double>(),
+                                           didx.as<int64_t>(), nullptr, ens_out.as<double>(), s, &ast)
+                    : turbda_ensf_analyze(&ap, ens.as<double>(), dy.as<double>(), dr.as<double>(),
+                                          didx.as<int64_t>(), ens_out.as<double>(), s, &ast);
             if (rc != TURBDA_OK) return aborted(k, ast.msg);
             toc(2);
             std::swap(ens.p, ens_out.p);

@@ -5,7 +5,7 @@ reference binding's ``run_experiment(config_json)`` / ``default_config_json``
 reference defaults.  Extra keys of this build: ``ensf.precision``
 ("fp32" | "fp64"), ``ensf.score_mode`` ("componentwise" | "joint"),
 ``obs.operator`` ("linear" | "arctan").  The whole cycle runs on the GPU
-(turbda_run_experiment); the variant "letkf" is not part of this build.
+(turbda_run_experiment), the LETKF variant included (turbda_letkf_analyze).
 """
 from __future__ import annotations
 
@@ -14,7 +14,8 @@ import json
 from . import capi
 from ._core import ConfigError
 
-_VARIANTS = {"free_run": capi.VARIANT_FREE_RUN, "ensf": capi.VARIANT_ENSF}
+_VARIANTS = {"free_run": capi.VARIANT_FREE_RUN, "letkf": capi.VARIANT_LETKF,
+             "ensf": capi.VARIANT_ENSF}
 
 
 def default_config() -> dict:
@@ -32,6 +33,8 @@ def default_config() -> dict:
                         "mixture": [{"probability": e.me_prob[c], "amplitude_fraction": e.me_frac[c]}
                                     for c in range(e.me_ncomp)]},
         "obs": {"r": e.obs_r, "thinning_stride": e.obs_thinning, "operator": "linear"},
+        "letkf": {"cutoff_km": e.letkf_cutoff_km, "domain_km": e.letkf_domain_km,
+                  "rtps_alpha": e.letkf_rtps_alpha, "obs_thinning": e.letkf_obs_thinning},
         "variant": "ensf", "model_quality": "perfect", "cycles": e.cycles,
         "obs_interval": e.obs_interval, "ensemble_size": e.ensemble_size, "seed": e.seed,
         "spinup_hours": e.spinup_hours, "clim_hours": e.clim_hours,
@@ -82,6 +85,10 @@ def to_struct(cfg: dict) -> "capi.Experiment":
     if "thinning_stride" in o:
         e.obs_thinning = o["thinning_stride"]
     e.obs_arctan = int(o.get("operator", "linear") == "arctan")
+    lk = cfg.get("letkf", {})
+    for k in ("cutoff_km", "domain_km", "rtps_alpha", "obs_thinning"):
+        if k in lk:
+            setattr(e, "letkf_" + k, lk[k])
     if "variant" in cfg:
         if cfg["variant"] not in _VARIANTS:
             raise ConfigError(f"unknown or unsupported variant '{cfg['variant']}'")

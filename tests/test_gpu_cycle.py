@@ -6,7 +6,8 @@ reference arm needs the GPU box too).
 Tolerances: the GPU SQG restates the reference's fp64 algorithm on the same
 FFT library (cuFFT under cuFFTW), so short integrations agree to ~1e-12;
 cycled runs with the fp64 faithful analysis agree to ~1e-9 over a few cycles
-(chaos amplifies rounding over time); the fp32 analysis is compared through
+(chaos amplifies rounding over time); the LETKF variant runs the reference
+driver with the Eigen-free LETKF restatement (oracle/letkf_restated.cpp); the fp32 analysis is compared through
 the time-mean analysis RMSE (north_star: "analysis RMSE against truth over a
 cycled SQG run must match within a stated tolerance"): 5 %.
 """
@@ -96,7 +97,10 @@ def test_sqg_rejects_bad_duration_and_blows_up(tb):
 
 
 @pytest.mark.parametrize("extra", [{}, {"model_quality": "imperfect"},
-                                   {"obs": {"thinning_stride": 4}}, {"variant": "free_run"}])
+                                   {"obs": {"thinning_stride": 4}}, {"variant": "free_run"},
+                                   {"variant": "letkf"},
+                                   {"variant": "letkf", "obs": {"thinning_stride": 3},
+                                    "letkf": {"cutoff_km": 3000.0, "rtps_alpha": 0.5}}])
 def test_run_experiment_fp64_vs_reference(tb, refc, extra):
     cfg = small_config(**extra)
     want = refc.run_experiment(cfg)
@@ -150,3 +154,15 @@ def test_run_experiment_fault_injection_like_reference(tb, refc):
         assert (rc is None) == (oc is None)
         if rc:
             assert rc.group(1) == oc.group(1)
+
+
+def test_letkf_cycle_beats_free_run(tb):
+    """proj/tests/test_osse.cpp:181-205: assimilation (LETKF) beats the free
+    run on its own forecasts."""
+    base = small_config(cycles=6, ensemble_size=8, model_quality="imperfect")
+    free = tb.run_experiment(json.dumps({**base, "variant": "free_run"}))
+    lk = tb.run_experiment(json.dumps({**base, "variant": "letkf"}))
+    mean = lambda rs: np.mean([r["analysis_rmse"] for r in rs])
+    assert mean(lk) < mean(free)
+    for r in lk:
+        assert np.isfinite(r["analysis_rmse"]) and r["analysis_spread"] > 0

@@ -130,3 +130,34 @@ def test_offsets_cover_each_cell_once():
         for ox, oy, gc in offs:
             ax, ay = min(abs(ox), n - abs(ox)), min(abs(oy), n - abs(oy))
             assert gc == L.gaspari_cohn(math.hypot(ax, ay) / cutoff)
+
+
+def _refcycle():
+    from oracle.oracle import HERE, RefCycleOracle
+    path = HERE / "_ref" / "libturbda_ref_cycle.so"
+    if not path.exists():
+        pytest.skip("oracle/_ref/libturbda_ref_cycle.so not built")
+    return RefCycleOracle()
+
+
+@pytest.mark.parametrize("n,m,stride,cutoff,alpha", [
+    (8, 6, 0, 2000.0, 0.3), (16, 20, 3, 2000.0, 0.0), (16, 9, 0, 1e12, 0.5), (32, 12, 4, 3000.0, 0.3),
+])
+def test_two_restatements_agree(n, m, stride, cutoff, alpha):
+    """numpy (per point, reference gather order) vs the Eigen-free C++
+    restatement running inside the reference's own types and parallel_for
+    (periodic-stencil gather order, Jacobi eigensolver)."""
+    rc = _refcycle()
+    d = 2 * n * n
+    x = gaussian_ensemble(m, d, 3 + n)
+    idx = None if stride == 0 else np.arange(0, d, stride, dtype=np.int64)
+    g = np.random.default_rng(4)
+    nobs = d if idx is None else idx.size
+    y = g.standard_normal(nobs)
+    r = 0.4 + g.random(nobs)
+    a = L.letkf_analyze(x, y, r, idx, n, n, cutoff_km=cutoff, rtps_alpha=alpha)
+    b = rc.letkf_analyze(x, y, r, idx, n, n, cutoff_km=cutoff, rtps_alpha=alpha, workers=4)
+    assert np.abs(a - b).max() <= 1e-10 * np.abs(a).max()
+    # the C++ restatement is bitwise independent of the worker count
+    assert np.array_equal(b, rc.letkf_analyze(x, y, r, idx, n, n, cutoff_km=cutoff,
+                                              rtps_alpha=alpha, workers=1))
