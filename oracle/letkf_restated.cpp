@@ -34,17 +34,16 @@ namespace {
 bool sym_eigen(std::vector<double> a, int m, std::vector<double>& lam, std::vector<double>& v) {
     v.assign(size_t(m) * m, 0.0);
     for (int i = 0; i < m; ++i) v[size_t(i) * m + i] = 1.0;
+    // rotations below double rounding (|a_pq| <= eps sqrt|a_pp a_qq|) are
+    // skipped; converged once a whole sweep skips every pair
     for (int sweep = 0; sweep < 60; ++sweep) {
-        double off = 0.0, dia = 0.0;
-        for (int i = 0; i < m; ++i)
-            for (int j = 0; j < m; ++j)
-                (i == j ? dia : off) += a[size_t(i) * m + j] * a[size_t(i) * m + j];
-        if (!(off > 1e-32 * dia)) break;
+        bool rotated = false;
         for (int p = 0; p < m - 1; ++p)
             for (int q = p + 1; q < m; ++q) {
                 const double apq = a[size_t(p) * m + q];
-                if (apq == 0.0) continue;
                 const double app = a[size_t(p) * m + p], aqq = a[size_t(q) * m + q];
+                if (!(std::fabs(apq) > 2.2e-16 * std::sqrt(std::fabs(app * aqq)))) continue;
+                rotated = true;
                 const double theta = (aqq - app) / (2.0 * apq);
                 const double t = std::fabs(theta) > 1e150
                                      ? 0.5 / theta
@@ -66,6 +65,7 @@ bool sym_eigen(std::vector<double> a, int m, std::vector<double>& lam, std::vect
                 }
                 a[size_t(p) * m + q] = a[size_t(q) * m + p] = 0.0;
             }
+        if (!rotated) break;
     }
     lam.resize(size_t(m));
     for (int i = 0; i < m; ++i) lam[size_t(i)] = a[size_t(i) * m + i];

@@ -28,6 +28,12 @@ namespace {
 
 std::atomic<uint64_t> g_launches{0};
 
+}  // namespace
+
+void tb200::add_launches(uint64_t n) { g_launches += n; }
+
+namespace {
+
 // Optional live timing of the fused analysis kernel (bench.py's roofline):
 // CUDA events recorded on the launching stream around each ensf launch.
 std::atomic<int> g_profile{0};

@@ -105,4 +105,7 @@ cudaError_t launch_joint_update(const KernelArgs& a, const double* x, const doub
 cudaError_t launch_diag(const double* x, int m, int64_t d, const double* truth, double* out,
                         cudaStream_t st);
 
+// evidence counter behind turbda_launch_count() (kernels of this library)
+void add_launches(uint64_t n);
+
 }  // namespace tb200

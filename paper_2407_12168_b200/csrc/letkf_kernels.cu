@@ -41,6 +41,7 @@
 #include <cuda_runtime.h>
 #include <cufft.h>
 
+#include "ensf_device.h"
 #include "turbda_b200.h"
 
 namespace tb200 {
@@ -236,24 +237,36 @@ struct PointArgs {
 };
 
 template <bool kVGlobal>
-__global__ void letkf_point_kernel(PointArgs a) {
+__global__ void __launch_bounds__(256) letkf_point_kernel(PointArgs a) {
     extern __shared__ double sm[];
     const int m = a.m;
     const int ld = m + 1;
     const int mp = m + (m & 1);  // even pairing size (a dummy index when m is odd)
     const int npairs = mp / 2;
+    const int nblk = npairs * (npairs + 1) / 2;
     double* A = sm;
     double* V = kVGlobal ? a.vscratch + size_t(blockIdx.x) * size_t(m) * ld : A + size_t(m) * ld;
-    double* rot = kVGlobal ? A + size_t(m) * ld : V + size_t(m) * ld;  // [npairs][2] c, s
-    int* pr = reinterpret_cast<int*>(rot + 2 * npairs);                // [npairs][2] p, q
-    double* vec = reinterpret_cast<double*>(pr + 2 * npairs + 2);      // 4 x m
+    double* rot = kVGlobal ? A + size_t(m) * ld : V + size_t(m) * ld;  // [npairs][3] c, s, t
+    double* vec = rot + 3 * npairs;                                     // 3 x m
     double* b = vec;
     double* u = vec + m;
     double* pert = vec + 2 * m;
-    double* red = vec + 3 * m;  // reduction scratch [blockDim / 32 + 2]
+    int* pr = reinterpret_cast<int*>(vec + 3 * m);   // [npairs][2] p, q of this round
+    int* blk = pr + 2 * npairs;                      // [nblk] (k1 << 16 | k2), k1 <= k2
+    int* rotated = blk + nblk;                       // any rotation this sweep
     const int tid = threadIdx.x, nt = blockDim.x;
     const int E = m * (m + 1) / 2;
     const double sm1 = sqrt(double(m - 1));
+    // loop strides over (pair, row) items without integer division
+    const int vi0 = tid % m, vk0 = tid / m, vdi = nt % m, vdk = nt / m;
+    for (int t = tid; t < nblk; t += nt) {
+        int k1 = 0, r = t;
+        while (r >= npairs - k1) {
+            r -= npairs - k1;
+            ++k1;
+        }
+        blk[t] = (k1 << 16) | (k1 + r);
+    }
 
     for (int64_t pt = blockIdx.x; pt < a.P; pt += gridDim.x) {
         const double count = a.fields[size_t(E + m) * a.P + pt];
@@ -267,44 +280,32 @@ __global__ void letkf_point_kernel(PointArgs a) {
             }
             continue;
         }
-        for (int t = tid; t < m * m; t += nt) {
-            const int i = t / m, j = t % m;
-            const double v = a.fields[size_t(tri(min(i, j), max(i, j), m)) * a.P + pt];
-            A[i * ld + j] = v + (i == j ? double(m - 1) : 0.0);
-            V[i * ld + j] = i == j ? 1.0 : 0.0;
+        for (int t = tid; t < E; t += nt) {
+            // upper-triangle field t -> (i, j), mirrored
+            int i = 0, r = t;
+            while (r >= m - i) {
+                r -= m - i;
+                ++i;
+            }
+            const int j = i + r;
+            const double v = a.fields[size_t(t) * a.P + pt] + (i == j ? double(m - 1) : 0.0);
+            A[i * ld + j] = v;
+            A[j * ld + i] = v;
         }
+        for (int t = tid; t < m * ld; t += nt) V[t] = 0.0;
         for (int t = tid; t < m; t += nt) b[t] = a.fields[size_t(E + t) * a.P + pt];
         __syncthreads();
+        for (int t = tid; t < m; t += nt) V[t * ld + t] = 1.0;
 
         // cyclic Jacobi, round-robin ordering: pair 0 = (r, mp-1), pair k =
-        // ((r+k) mod (mp-1), (r-k) mod (mp-1)); rounds of disjoint rotations
+        // ((r+k) mod (mp-1), (r-k) mod (mp-1)); a round applies its mp/2
+        // disjoint rotations at once as A <- J^T A J, one 2x2 block of A per
+        // thread-item (upper blocks, mirrored), and V <- V J.  A rotation is
+        // skipped when |a_pq| <= eps sqrt(|a_pp a_qq|) (below double
+        // rounding); converged = a sweep without one.
         for (int sweep = 0; sweep < a.max_sweeps; ++sweep) {
-            // convergence: off-diagonal mass relative to the diagonal
-            double off = 0.0, dia = 0.0;
-            for (int t = tid; t < m * m; t += nt) {
-                const int i = t / m, j = t % m;
-                const double v = A[i * ld + j];
-                if (i == j) dia += v * v;
-                else off += v * v;
-            }
-            for (int o = 16; o; o >>= 1) {
-                off += __shfl_xor_sync(0xffffffffu, off, o);
-                dia += __shfl_xor_sync(0xffffffffu, dia, o);
-            }
-            if ((tid & 31) == 0) {
-                red[2 * (tid >> 5)] = off;
-                red[2 * (tid >> 5) + 1] = dia;
-            }
+            if (tid == 0) *rotated = 0;
             __syncthreads();
-            off = 0.0;
-            dia = 0.0;
-            for (int w = 0; w < nt / 32; ++w) {
-                off += red[2 * w];
-                dia += red[2 * w + 1];
-            }
-            __syncthreads();
-            if (!(off > 1e-32 * dia)) break;
-
             for (int rnd = 0; rnd < mp - 1; ++rnd) {
                 for (int k = tid; k < npairs; k += nt) {
                     int p, q;
@@ -312,61 +313,101 @@ __global__ void letkf_point_kernel(PointArgs a) {
                         p = rnd;
                         q = mp - 1;
                     } else {
-                        p = (rnd + k) % (mp - 1);
-                        q = (rnd - k + (mp - 1)) % (mp - 1);
+                        p = rnd + k;
+                        p -= p >= mp - 1 ? mp - 1 : 0;
+                        q = rnd - k;
+                        q += q < 0 ? mp - 1 : 0;
                     }
                     if (p > q) {
                         const int t = p;
                         p = q;
                         q = t;
                     }
-                    double c = 1.0, s = 0.0;
+                    double c = 1.0, s = 0.0, tt = 0.0;
                     if (q < m) {
                         const double apq = A[p * ld + q];
-                        if (apq != 0.0) {
-                            const double app = A[p * ld + p], aqq = A[q * ld + q];
-                            const double theta = (aqq - app) / (2.0 * apq);
-                            double t;
-                            if (fabs(theta) > 1e150) t = 0.5 / theta;
-                            else t = copysign(1.0, theta) / (fabs(theta) + sqrt(theta * theta + 1.0));
-                            c = 1.0 / sqrt(t * t + 1.0);
-                            s = t * c;
+                        const double app = A[p * ld + p], aqq = A[q * ld + q];
+                        if (fabs(apq) > 2.2e-16 * sqrt(fabs(app * aqq))) {
+                            *rotated = 1;
+                            // t = tan(phi) = sign(h) g / (|h| + sqrt(h^2 + g^2)),
+                            // h = a_qq - a_pp, g = 2 a_pq (the small root)
+                            const double h = aqq - app, g = 2.0 * apq;
+                            tt = (h < 0.0 ? -g : g) / (fabs(h) + sqrt(fma(h, h, g * g)));
+                            c = rsqrt(fma(tt, tt, 1.0));
+                            s = tt * c;
                         }
                     }
-                    rot[2 * k] = c;
-                    rot[2 * k + 1] = s;
+                    rot[3 * k] = c;
+                    rot[3 * k + 1] = s;
+                    rot[3 * k + 2] = tt;
                     pr[2 * k] = p;
                     pr[2 * k + 1] = q;
                 }
                 __syncthreads();
-                // A <- A J and V <- V J (columns p, q of every pair)
-                for (int t = tid; t < npairs * m; t += nt) {
-                    const int k = t / m, i = t % m;
-                    const int p = pr[2 * k], q = pr[2 * k + 1];
-                    const double s = rot[2 * k + 1];
-                    if (q >= m || s == 0.0) continue;
-                    const double c = rot[2 * k];
-                    const double ap = A[i * ld + p], aq = A[i * ld + q];
-                    A[i * ld + p] = c * ap - s * aq;
-                    A[i * ld + q] = s * ap + c * aq;
-                    const double vp = V[i * ld + p], vq = V[i * ld + q];
-                    V[i * ld + p] = c * vp - s * vq;
-                    V[i * ld + q] = s * vp + c * vq;
+                // A <- J^T A J on 2x2 blocks (rows of pair k1, columns of pair k2)
+                for (int t = tid; t < nblk; t += nt) {
+                    const int k1 = blk[t] >> 16, k2 = blk[t] & 0xffff;
+                    const double s1 = rot[3 * k1 + 1], s2 = rot[3 * k2 + 1];
+                    if (s1 == 0.0 && s2 == 0.0) continue;
+                    const int p1 = pr[2 * k1], q1 = pr[2 * k1 + 1];
+                    const int p2 = pr[2 * k2], q2 = pr[2 * k2 + 1];
+                    if (k1 == k2) {
+                        // the annihilated pair: closed form (a_pq -> 0)
+                        const double tt = rot[3 * k1 + 2], apq = A[p1 * ld + q1];
+                        A[p1 * ld + p1] -= tt * apq;
+                        A[q1 * ld + q1] += tt * apq;
+                        A[p1 * ld + q1] = 0.0;
+                        A[q1 * ld + p1] = 0.0;
+                        continue;
+                    }
+                    const double c1 = rot[3 * k1], c2 = rot[3 * k2];
+                    const bool r1 = q1 < m, r2 = q2 < m;
+                    const double x11 = A[p1 * ld + p2];
+                    const double x12 = r2 ? A[p1 * ld + q2] : 0.0;
+                    const double x21 = r1 ? A[q1 * ld + p2] : 0.0;
+                    const double x22 = (r1 && r2) ? A[q1 * ld + q2] : 0.0;
+                    // columns (J2), then rows (J1^T)
+                    const double y11 = c2 * x11 - s2 * x12, y12 = s2 * x11 + c2 * x12;
+                    const double y21 = c2 * x21 - s2 * x22, y22 = s2 * x21 + c2 * x22;
+                    const double z11 = c1 * y11 - s1 * y21, z21 = s1 * y11 + c1 * y21;
+                    const double z12 = c1 * y12 - s1 * y22, z22 = s1 * y12 + c1 * y22;
+                    A[p1 * ld + p2] = z11;
+                    A[p2 * ld + p1] = z11;
+                    if (r2) {
+                        A[p1 * ld + q2] = z12;
+                        A[q2 * ld + p1] = z12;
+                    }
+                    if (r1) {
+                        A[q1 * ld + p2] = z21;
+                        A[p2 * ld + q1] = z21;
+                    }
+                    if (r1 && r2) {
+                        A[q1 * ld + q2] = z22;
+                        A[q2 * ld + q1] = z22;
+                    }
                 }
-                __syncthreads();
-                // A <- J^T A (rows p, q); the annihilated pair is set to 0
-                for (int t = tid; t < npairs * m; t += nt) {
-                    const int k = t / m, j = t % m;
-                    const int p = pr[2 * k], q = pr[2 * k + 1];
-                    const double s = rot[2 * k + 1];
-                    if (q >= m || s == 0.0) continue;
-                    const double c = rot[2 * k];
-                    const double ap = A[p * ld + j], aq = A[q * ld + j];
-                    A[p * ld + j] = (j == q) ? 0.0 : c * ap - s * aq;
-                    A[q * ld + j] = (j == p) ? 0.0 : s * ap + c * aq;
+                // V <- V J (rows i, columns p, q of every pair)
+                for (int i = vi0, k = vk0; k < npairs;) {
+                    const double s = rot[3 * k + 1];
+                    const int q = pr[2 * k + 1];
+                    if (s != 0.0 && q < m) {
+                        const int p = pr[2 * k];
+                        const double c = rot[3 * k];
+                        const double vp = V[i * ld + p], vq = V[i * ld + q];
+                        V[i * ld + p] = c * vp - s * vq;
+                        V[i * ld + q] = s * vp + c * vq;
+                    }
+                    i += vdi;
+                    k += vdk;
+                    if (i >= m) {
+                        i -= m;
+                        ++k;
+                    }
                 }
                 __syncthreads();
             }
+            if (*rotated == 0) break;
+            __syncthreads();
         }
         // eigenvalues on the diagonal; a non-positive or non-finite one is a
         // SingularAnalysisError (proj/src/letkf.cpp:40-44)
@@ -416,6 +457,226 @@ __global__ void letkf_point_kernel(PointArgs a) {
                 double s = 0.0;
                 for (int k = 0; k < m; ++k) s += V[j * ld + k] * u[k];
                 a.out[size_t(j) * a.d + row] = mean + wx + sm1 * s;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// 5'. M <= 64: the transform without an eigendecomposition.  ETKF needs
+// only A^-1 b and W = sqrt(M-1) A^-1/2 (proj/src/letkf.cpp:46-53): with
+// B = A / c the coupled Newton-Schulz iteration
+//     T = 3I - Z Y,   Y <- Y T / 2,   Z <- T Z / 2     (Y0 = B, Z0 = I)
+// converges quadratically to Y = B^1/2, Z = B^-1/2 whenever the spectrum of
+// B lies in (0, 2).  A >= (M-1) I and lambda_max <= ||A||_inf, so
+// c = (M-1 + ||A||_inf) / 2 qualifies, and the iteration count follows from
+// the scalar recurrence p <- p (3 - p)^2 / 4 at both spectrum ends.  Every
+// product is a 64 x 64 x 64 fp64 GEMM on the FP64 tensor cores
+// (DMMA.8x8x4): ~10 iterations x 3 GEMMs replace ~570 Jacobi rounds.
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+// acc = X Y for this warp's block of 2 x 4 8x8 tiles (rows 16 br.., cols 32 bc..)
+__device__ __forceinline__ void warp_gemm(const double* X, const double* Y, int mp, int ld,
+                                          int br, int bc, int lane, double (&acc)[2][4][2]) {
+    const int nt8 = mp >> 3;
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[r][q][0] = acc[r][q][1] = 0.0;
+    const int lr = lane >> 2, lk = lane & 3;
+    for (int k0 = 0; k0 < mp; k0 += 4) {
+        const int kk = k0 + lk;
+        double av[2], bv[4];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int tr = 2 * br + r;
+            av[r] = tr < nt8 ? X[(8 * tr + lr) * ld + kk] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int tc = 4 * bc + q;
+            bv[q] = tc < nt8 ? Y[kk * ld + 8 * tc + lr] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (2 * br + r < nt8 && 4 * bc + q < nt8) dmma884(acc[r][q], av[r], bv[q]);
+    }
+}
+
+// out = alpha * acc + beta * I over the warp's block
+__device__ __forceinline__ void warp_store(double* out, int mp, int ld, int br, int bc, int lane,
+                                           const double (&acc)[2][4][2], double alpha,
+                                           double beta) {
+    const int nt8 = mp >> 3;
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (2 * br + r >= nt8 || 4 * bc + q >= nt8) continue;
+            const int row = 8 * (2 * br + r) + (lane >> 2);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = 8 * (4 * bc + q) + 2 * (lane & 3) + e;
+                out[row * ld + col] = alpha * acc[r][q][e] + (row == col ? beta : 0.0);
+            }
+        }
+}
+
+__global__ void __launch_bounds__(256) letkf_point_ns_kernel(PointArgs a) {
+    extern __shared__ double sm[];
+    const int m = a.m;
+    const int mp = (m + 7) & ~7;
+    const int ld = mp + 4;
+    double* Y = sm;
+    double* Z = Y + size_t(mp) * ld;
+    double* T = Z + size_t(mp) * ld;
+    double* vec = T + size_t(mp) * ld;  // b, u, pert, wbar [mp] each + reduction
+    double* b = vec;
+    double* u = vec + mp;
+    double* pert = vec + 2 * mp;
+    double* wbar = vec + 3 * mp;
+    double* red = vec + 4 * mp;  // [8]
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int nt8 = mp >> 3, nbr = (nt8 + 1) / 2, nbc = (nt8 + 3) / 4;
+    const bool gw = warp < nbr * nbc;  // warp owns a GEMM block
+    const int br = gw ? warp / nbc : 0, bc = gw ? warp % nbc : 0;
+    const int E = m * (m + 1) / 2;
+    const double sm1 = sqrt(double(m - 1));
+
+    for (int64_t pt = blockIdx.x; pt < a.P; pt += gridDim.x) {
+        const double count = a.fields[size_t(E + m) * a.P + pt];
+        const int64_t row0 = pt, row1 = a.P + pt;
+        if (!(count > 0.5)) {
+            for (int j = tid; j < m; j += nt) {
+                a.out[size_t(j) * a.d + row0] = a.x[size_t(j) * a.d + row0];
+                a.out[size_t(j) * a.d + row1] = a.x[size_t(j) * a.d + row1];
+            }
+            continue;
+        }
+        // A (mirrored upper fields) into T; padded rows/cols: identity
+        for (int t = tid; t < mp * mp; t += nt) {
+            const int i = t / mp, j = t - (t / mp) * mp;
+            double v;
+            if (i < m && j < m) {
+                const int lo = min(i, j), hi = max(i, j);
+                const int f = lo * m - (lo * (lo - 1)) / 2 + (hi - lo);
+                v = a.fields[size_t(f) * a.P + pt] + (i == j ? double(m - 1) : 0.0);
+            } else {
+                v = i == j ? 1.0 : 0.0;
+            }
+            T[i * ld + j] = v;
+        }
+        for (int t = tid; t < mp; t += nt) b[t] = t < m ? a.fields[size_t(E + t) * a.P + pt] : 0.0;
+        __syncthreads();
+        // ||A||_inf (max absolute row sum)
+        double rs = 0.0;
+        for (int i = tid; i < m; i += nt) {
+            double s = 0.0;
+            for (int j = 0; j < m; ++j) s += fabs(T[i * ld + j]);
+            rs = fmax(rs, s);
+        }
+        for (int o = 16; o; o >>= 1) rs = fmax(rs, __shfl_xor_sync(0xffffffffu, rs, o));
+        if (lane == 0) red[warp] = rs;
+        __syncthreads();
+        double ainf = 0.0;
+        for (int w = 0; w < nt / 32; ++w) ainf = fmax(ainf, red[w]);
+        const double cs = 0.5 * (double(m - 1) + ainf);
+        const double inv_c = 1.0 / cs;
+        // Y0 = B = A / c (padding keeps eigenvalue 1), Z0 = I
+        for (int t = tid; t < mp * mp; t += nt) {
+            const int i = t / mp, j = t - (t / mp) * mp;
+            const bool pad = i >= m || j >= m;
+            Y[i * ld + j] = pad ? T[i * ld + j] : T[i * ld + j] * inv_c;
+            Z[i * ld + j] = i == j ? 1.0 : 0.0;
+        }
+        const bool finite = isfinite(cs) && cs > 0.0;
+        __syncthreads();
+        // iterate until ||Z Y - I||_max <= 1e-10 (the next update squares the
+        // error below double rounding), at most 60 times; the final
+        // iteration skips the Y update nobody reads
+        double acc[2][4][2];
+        for (int it = 0; finite && it < 60; ++it) {
+            // T = 3I - Z Y, with the residual max |T - 2I| = max |Z Y - I|
+            double res = 0.0;
+            if (gw) {
+                warp_gemm(Z, Y, mp, ld, br, bc, lane, acc);
+                warp_store(T, mp, ld, br, bc, lane, acc, -1.0, 3.0);
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int row = 8 * (2 * br + r) + (lane >> 2);
+                            const int col = 8 * (4 * bc + q) + 2 * (lane & 3) + e;
+                            if (row < mp && col < mp)
+                                res = fmax(res, fabs(acc[r][q][e] - (row == col ? 1.0 : 0.0)));
+                        }
+            }
+            for (int o = 16; o; o >>= 1) res = fmax(res, __shfl_xor_sync(0xffffffffu, res, o));
+            if (lane == 0) red[warp] = res;
+            __syncthreads();
+            res = 0.0;
+            for (int w = 0; w < nt / 32; ++w) res = fmax(res, red[w]);
+            const bool last = !(res > 1e-10);  // (fmax drops NaN: caught below)
+            if (!last) {
+                // Y <- Y T / 2 (in place once every warp has read Y)
+                if (gw) warp_gemm(Y, T, mp, ld, br, bc, lane, acc);
+                __syncthreads();
+                if (gw) warp_store(Y, mp, ld, br, bc, lane, acc, 0.5, 0.0);
+            }
+            // Z <- T Z / 2
+            if (gw) warp_gemm(T, Z, mp, ld, br, bc, lane, acc);
+            __syncthreads();
+            if (gw) warp_store(Z, mp, ld, br, bc, lane, acc, 0.5, 0.0);
+            __syncthreads();
+            if (last) break;
+        }
+        // A^-1/2 = Z / sqrt(c); a non-finite transform is a
+        // SingularAnalysisError (proj/src/letkf.cpp:40-44)
+        bool bad = !finite;
+        for (int t = tid; t < m * m && !bad; t += nt) {
+            const int i = t / m, j = t - (t / m) * m;
+            if (!isfinite(Z[i * ld + j])) bad = true;
+        }
+        if (__syncthreads_or(bad)) {
+            if (tid == 0) atomicMin(a.singular, (unsigned long long)pt);
+            continue;
+        }
+        const double isc = rsqrt(cs);
+        // wbar = A^-1 b = (Z (Z b)) / c
+        for (int i = tid; i < m; i += nt) {
+            double s = 0.0;
+            for (int k = 0; k < m; ++k) s += Z[i * ld + k] * b[k];
+            u[i] = s;
+        }
+        __syncthreads();
+        for (int i = tid; i < m; i += nt) {
+            double s = 0.0;
+            for (int k = 0; k < m; ++k) s += Z[i * ld + k] * u[k];
+            wbar[i] = s * inv_c;
+        }
+        __syncthreads();
+        // both levels with the same transform (proj/src/letkf.cpp:162-171)
+        for (int lev = 0; lev < 2; ++lev) {
+            const int64_t row = lev ? row1 : row0;
+            double mean = 0.0;
+            for (int j = 0; j < m; ++j) mean += a.x[size_t(j) * a.d + row];
+            mean *= 1.0 / double(m);
+            for (int j = tid; j < m; j += nt) pert[j] = a.x[size_t(j) * a.d + row] - mean;
+            __syncthreads();
+            double wx = 0.0;
+            for (int k = 0; k < m; ++k) wx += pert[k] * wbar[k];
+            for (int j = tid; j < m; j += nt) {
+                double s = 0.0;
+                for (int k = 0; k < m; ++k) s += Z[j * ld + k] * pert[k];
+                a.out[size_t(j) * a.d + row] = mean + wx + sm1 * (s * isc);
             }
             __syncthreads();
         }
@@ -697,6 +958,7 @@ int turbda_letkf_analyze(const turbda_letkf_params* p, const double* forecast, c
             w->yb.as<double>(), w->dinn.as<double>(), w->rinv.as<double>(),
             w->cell.as<uint32_t>(), w->order.as<uint32_t>());
         LK_CUDA(cudaGetLastError());
+        add_launches(2);
         count_cells_kernel<<<blocks_for(nobs, 256), 256, 0, s>>>(w->cell.as<uint32_t>(), nobs,
                                                                   w->count.as<int>());
         LK_CUDA(cudaGetLastError());
@@ -735,6 +997,7 @@ int turbda_letkf_analyze(const turbda_letkf_params* p, const double* forecast, c
             w->sorted_obs.as<uint32_t>(), w->start.as<int>(), nobs, m, P, nf,
             w->fields.as<double>());
         LK_CUDA(cudaGetLastError());
+        add_launches(1);
     }
     // 4. localization = periodic convolution with the Gaspari-Cohn stencil
     const double cutoff = p->cutoff_km / p->domain_km * double(n);
@@ -749,6 +1012,7 @@ int turbda_letkf_analyze(const turbda_letkf_params* p, const double* forecast, c
         spectral_scale_kernel<<<blocks_for(total, 256), 256, 0, s>>>(g, khat, nh, total, f0,
                                                                       nf - 1);
         LK_CUDA(cudaGetLastError());
+        add_launches(1);
         LK_FFT(cufftExecZ2D(w->z2d, g, fb));
     }
     // 5. per-point eigensolve + transform
@@ -757,11 +1021,36 @@ int turbda_letkf_analyze(const turbda_letkf_params* p, const double* forecast, c
         const int npairs = (m + (m & 1)) / 2;
         const size_t ld = size_t(m) + 1;
         const size_t mat = sizeof(double) * size_t(m) * ld;
-        const size_t extra = sizeof(double) * 2 * npairs + sizeof(int) * (2 * npairs + 2) +
-                             sizeof(double) * (4 * size_t(m) + threads / 32 * 2 + 2);
+        const size_t nblk = size_t(npairs) * (npairs + 1) / 2;
+        const size_t extra = sizeof(double) * (3 * size_t(npairs) + 3 * size_t(m)) +
+                             sizeof(int) * (2 * size_t(npairs) + nblk + 2);
         int dev_smem = 0, nsm = 0;
         LK_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         LK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        if (m <= 64) {
+            // tensor-core Newton-Schulz transform
+            const int mp = (m + 7) & ~7;
+            const size_t smem_ns = sizeof(double) * (3 * size_t(mp) * (mp + 4) + 4 * size_t(mp) + 8);
+            PointArgs pn{};
+            pn.fields = w->fields.as<double>();
+            pn.P = P;
+            pn.m = m;
+            pn.nx = n;
+            pn.ny = n;
+            pn.d = d;
+            pn.x = dx;
+            pn.out = dout;
+            pn.singular = w->singular.as<unsigned long long>();
+            LK_CUDA(cudaFuncSetAttribute(letkf_point_ns_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_ns)));
+            int per_sm_ns = 0;
+            LK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_ns, letkf_point_ns_kernel,
+                                                                  256, smem_ns));
+            const int64_t grid_ns = std::min<int64_t>(P, int64_t(std::max(per_sm_ns, 1)) * nsm);
+            letkf_point_ns_kernel<<<unsigned(grid_ns), 256, smem_ns, s>>>(pn);
+            LK_CUDA(cudaGetLastError());
+            add_launches(1);
+        } else {
         const bool vglobal = 2 * mat + extra + 64 > size_t(dev_smem);
         const size_t smem = (vglobal ? mat : 2 * mat) + extra + 64;
         if (smem > size_t(dev_smem))
@@ -776,7 +1065,7 @@ int turbda_letkf_analyze(const turbda_letkf_params* p, const double* forecast, c
         pa.x = dx;
         pa.out = dout;
         pa.singular = w->singular.as<unsigned long long>();
-        pa.max_sweeps = 30;
+        pa.max_sweeps = 40;
         int per_sm = 0;
         if (vglobal) {
             LK_CUDA(cudaFuncSetAttribute(letkf_point_kernel<true>,
@@ -798,11 +1087,14 @@ int turbda_letkf_analyze(const turbda_letkf_params* p, const double* forecast, c
             letkf_point_kernel<false><<<unsigned(grid), threads, smem, s>>>(pa);
         }
         LK_CUDA(cudaGetLastError());
+        add_launches(1);
+        }
     }
     // 6. RTPS (alpha == 0 or a single member: the analysis is returned as is)
     if (p->rtps_alpha != 0.0 && m >= 2) {
         rtps_kernel<<<blocks_for(d, 256), 256, 0, s>>>(dout, dx, m, d, p->rtps_alpha);
         LK_CUDA(cudaGetLastError());
+        add_launches(1);
     }
     unsigned long long sing = 0;
     LK_CUDA(cudaMemcpyAsync(&sing, w->singular.p, sizeof(sing), cudaMemcpyDeviceToHost, s));
@@ -854,6 +1146,7 @@ int turbda_rtps_inflate(const double* analysis, const double* background, int32_
     if (alpha != 0.0 && m >= 2 && d > 0) {
         rtps_kernel<<<blocks_for(d, 256), 256, 0, s>>>(o, bg, m, d, alpha);
         LK_CUDA(cudaGetLastError());
+        add_launches(1);
     }
     if (!on_dev) LK_CUDA(cudaMemcpyAsync(out, o, sizeof(double) * md, cudaMemcpyDeviceToHost, s));
     LK_CUDA(cudaStreamSynchronize(s));

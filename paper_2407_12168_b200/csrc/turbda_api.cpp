@@ -17,6 +17,7 @@
 #include "turbda/ensemble.hpp"
 #include "turbda/ensf.hpp"
 #include "turbda/errors.hpp"
+#include "turbda/letkf.hpp"
 #include "turbda/observation.hpp"
 #include "turbda/parallel.hpp"
 #include "turbda/rng.hpp"
@@ -32,6 +33,7 @@ namespace {
         case TURBDA_DIMENSION: throw DimensionError(st.msg);
         case TURBDA_DIVERGED: throw SamplerDivergedError(st.diverged_t);
         case TURBDA_DOMAIN: throw std::domain_error(st.msg);
+        case TURBDA_SINGULAR: throw SingularAnalysisError(st.diverged_particle, st.diverged_step);
         default: throw std::runtime_error(std::string("turbda_b200: ") + st.msg);
     }
 }
@@ -412,6 +414,80 @@ Ensemble relax_spread(const Ensemble& analysis, const Ensemble& forecast, double
     std::vector<double> o(a.size());
     turbda_status st{};
     check(turbda_relax_spread(a.data(), f.data(), analysis.size(), int64_t(analysis.dim()), factor,
+                              o.data(), -1, 0u, nullptr, &st),
+          st);
+    Ensemble out = analysis;
+    const std::size_t d = analysis.dim();
+    for (int j = 0; j < out.size(); ++j)
+        std::copy(o.begin() + std::ptrdiff_t(size_t(j) * d), o.begin() + std::ptrdiff_t(size_t(j + 1) * d),
+                  out.members[size_t(j)].begin());
+    return out;
+}
+
+// -------------------------------------------------------------- letkf -----
+double gaspari_cohn(double r) {
+    double v = 0.0;
+    turbda_status st{};
+    check(turbda_gaspari_cohn(r, &v, &st), st);
+    return v;
+}
+
+Ensemble letkf_analyze(const Ensemble& forecast, const Observation& obs, const LetkfConfig& cfg,
+                       const GridSpec& grid, int /*workers: the GPU grid*/) {
+    // validation order of proj/src/letkf.cpp:57-69
+    forecast.validate();
+    obs.validate();
+    cfg.validate();
+    grid.validate();
+    if (grid.nx != grid.ny || grid.lx != grid.ly)
+        throw ConfigError("letkf_analyze: isotropic metric needs nx == ny");
+    if (std::fabs(forecast.valid_time - obs.time) > 1e-6)
+        throw ConfigError("letkf_analyze: forecast/observation time mismatch");
+    const std::size_t d = forecast.dim();
+    if (d != grid.grid_size() || obs.op.state_dim != d)
+        throw DimensionError("letkf_analyze: state/grid size mismatch");
+
+    turbda_letkf_params p;
+    turbda_letkf_params_init(&p);
+    p.nx = grid.nx;
+    p.ny = grid.ny;
+    p.n_members = forecast.size();
+    p.obs_kind = abi_kind(obs.op.kind);
+    p.obs_dim = int64_t(obs.y.size());
+    p.cutoff_km = cfg.cutoff_km;
+    p.domain_km = cfg.domain_km;
+    p.rtps_alpha = cfg.rtps_alpha;
+    const FlatObs fo = flatten_obs(obs);
+    std::vector<double> locs(2 * obs.locations.size());
+    for (std::size_t k = 0; k < obs.locations.size(); ++k) {
+        locs[2 * k] = obs.locations[k][0];
+        locs[2 * k + 1] = obs.locations[k][1];
+    }
+    const std::vector<double> x = pack(forecast);
+    std::vector<double> o(x.size());
+    turbda_status st{};
+    check(turbda_letkf_analyze(&p, x.data(), obs.y.data(), obs.r_diag.data(),
+                               fo.idx.empty() ? nullptr : fo.idx.data(),
+                               locs.empty() ? nullptr : locs.data(), o.data(), nullptr, &st),
+          st);
+    Ensemble out = forecast;
+    for (int j = 0; j < out.size(); ++j)
+        std::copy(o.begin() + std::ptrdiff_t(size_t(j) * d), o.begin() + std::ptrdiff_t(size_t(j + 1) * d),
+                  out.members[size_t(j)].begin());
+    return out;
+}
+
+Ensemble rtps_inflate(const Ensemble& analysis, const Ensemble& background, double alpha) {
+    if (alpha == 0.0) return analysis;
+    analysis.validate(false);
+    background.validate(false);
+    if (analysis.size() != background.size() || analysis.dim() != background.dim())
+        throw DimensionError("rtps_inflate: shape mismatch");
+    if (analysis.size() < 2) return analysis;
+    const std::vector<double> a = pack(analysis), b = pack(background);
+    std::vector<double> o(a.size());
+    turbda_status st{};
+    check(turbda_rtps_inflate(a.data(), b.data(), analysis.size(), int64_t(analysis.dim()), alpha,
                               o.data(), -1, 0u, nullptr, &st),
           st);
     Ensemble out = analysis;

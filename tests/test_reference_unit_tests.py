@@ -50,3 +50,29 @@ def test_reference_suite_on_b200():
     print(out[-3000:])
     assert len(passed) + len(failed) == 38
     assert failed == EXPECTED_FAILURES, out
+
+
+CPP_LETKF = ROOT / "tests" / "cpp" / "_build" / "test_cpp_letkf"
+
+
+def _run_cpp_letkf(filt=None):
+    if not CPP_LETKF.exists():
+        pytest.skip("tests/cpp/_build/test_cpp_letkf not built (make -C tests/cpp)")
+    cmd = [str(CPP_LETKF)] + ([filt] if filt else [])
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+
+
+def test_cpp_letkf_api_host_cases():
+    """gaspari_cohn and the argument checks of the C++ LETKF API need no GPU."""
+    for filt in ("gaspari_cohn", "input validation"):
+        r = _run_cpp_letkf(filt)
+        assert r.returncode == 0, r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_letkf_api_on_b200():
+    """The Eigen-free cases of proj/tests/test_letkf.cpp against the C++ API
+    (include/turbda/letkf.hpp) on the GPU."""
+    r = _run_cpp_letkf()
+    print(r.stdout[-3000:])
+    assert r.returncode == 0 and "failed=0" in r.stdout, r.stdout
