@@ -479,59 +479,80 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
-// acc = X Y for this warp's block of 2 x 4 8x8 tiles (rows 16 br.., cols 32 bc..)
-__device__ __forceinline__ void warp_gemm(const double* X, const double* Y, int mp, int ld,
-                                          int br, int bc, int lane, double (&acc)[2][4][2]) {
-    const int nt8 = mp >> 3;
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[r][q][0] = acc[r][q][1] = 0.0;
-    const int lr = lane >> 2, lk = lane & 3;
-    for (int k0 = 0; k0 < mp; k0 += 4) {
-        const int kk = k0 + lk;
-        double av[2], bv[4];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int tr = 2 * br + r;
-            av[r] = tr < nt8 ? X[(8 * tr + lr) * ld + kk] : 0.0;
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int tc = 4 * bc + q;
-            bv[q] = tc < nt8 ? Y[kk * ld + 8 * tc + lr] : 0.0;
-        }
+// C = X Y for the Newton-Schulz iterates: warp w owns one block of 2 x 4
+// tiles (8 x 8 each) of the output, accumulators in registers until the
+// caller's barrier, so C may overwrite X or Y.  The full product is formed:
+// the iterates are symmetric in exact arithmetic, but mirroring the upper
+// triangle breaks the coupled iteration's self-correction and diverges for
+// condition numbers >= 1e4 (measured on the numpy model of this kernel).
+template <int NT8>
+struct NsGemm {
+    static constexpr int nbr = (NT8 + 1) / 2, nbc = (NT8 + 3) / 4;
+    bool own;
+    int br, bc;
+    double acc[2][4][2];
+
+    __device__ __forceinline__ void setup(int warp) {
+        own = warp < nbr * nbc;
+        br = own ? warp / nbc : 0;
+        bc = own ? warp % nbc : 0;
+    }
+
+    __device__ __forceinline__ void compute(const double* X, const double* Y, int ld, int lane) {
+        constexpr int mp = 8 * NT8;
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
+            for (int q = 0; q < 4; ++q) acc[r][q][0] = acc[r][q][1] = 0.0;
+        if (!own) return;
+        const int lr = lane >> 2, lk = lane & 3;
+#pragma unroll 4
+        for (int k0 = 0; k0 < mp; k0 += 4) {
+            const int kk = k0 + lk;
+            double av[2], bv[4];
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+                av[r] = 2 * br + r < NT8 ? X[(16 * br + 8 * r + lr) * ld + kk] : 0.0;
+#pragma unroll
             for (int q = 0; q < 4; ++q)
-                if (2 * br + r < nt8 && 4 * bc + q < nt8) dmma884(acc[r][q], av[r], bv[q]);
-    }
-}
-
-// out = alpha * acc + beta * I over the warp's block
-__device__ __forceinline__ void warp_store(double* out, int mp, int ld, int br, int bc, int lane,
-                                           const double (&acc)[2][4][2], double alpha,
-                                           double beta) {
-    const int nt8 = mp >> 3;
+                bv[q] = 4 * bc + q < NT8 ? Y[kk * ld + 32 * bc + 8 * q + lr] : 0.0;
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+            for (int r = 0; r < 2; ++r)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (2 * br + r >= nt8 || 4 * bc + q >= nt8) continue;
-            const int row = 8 * (2 * br + r) + (lane >> 2);
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int col = 8 * (4 * bc + q) + 2 * (lane & 3) + e;
-                out[row * ld + col] = alpha * acc[r][q][e] + (row == col ? beta : 0.0);
-            }
+                for (int q = 0; q < 4; ++q) dmma884(acc[r][q], av[r], bv[q]);
         }
-}
+    }
 
+    // C = alpha acc + beta I; returns the local max |acc - I| (the
+    // Newton-Schulz residual when X Y ~ I)
+    __device__ __forceinline__ double store(double* C, int ld, int lane, double alpha,
+                                            double beta) const {
+        double res = 0.0;
+        if (!own) return res;
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int tr = 2 * br + r, tc = 4 * bc + q;
+                if (tr >= NT8 || tc >= NT8) continue;
+                const int row = 8 * tr + (lane >> 2);
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int col = 8 * tc + 2 * (lane & 3) + e;
+                    const double v = acc[r][q][e];
+                    res = fmax(res, fabs(v - (row == col ? 1.0 : 0.0)));
+                    C[row * ld + col] = alpha * v + (row == col ? beta : 0.0);
+                }
+            }
+        return res;
+    }
+};
+
+template <int NT8>
 __global__ void __launch_bounds__(256) letkf_point_ns_kernel(PointArgs a) {
     extern __shared__ double sm[];
     const int m = a.m;
-    const int mp = (m + 7) & ~7;
+    constexpr int mp = 8 * NT8;
     const int ld = mp + 4;
     double* Y = sm;
     double* Z = Y + size_t(mp) * ld;
@@ -543,9 +564,8 @@ __global__ void __launch_bounds__(256) letkf_point_ns_kernel(PointArgs a) {
     double* wbar = vec + 3 * mp;
     double* red = vec + 4 * mp;  // [8]
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-    const int nt8 = mp >> 3, nbr = (nt8 + 1) / 2, nbc = (nt8 + 3) / 4;
-    const bool gw = warp < nbr * nbc;  // warp owns a GEMM block
-    const int br = gw ? warp / nbc : 0, bc = gw ? warp % nbc : 0;
+    NsGemm<NT8> g;
+    g.setup(warp);
     const int E = m * (m + 1) / 2;
     const double sm1 = sqrt(double(m - 1));
 
@@ -600,25 +620,10 @@ __global__ void __launch_bounds__(256) letkf_point_ns_kernel(PointArgs a) {
         // iterate until ||Z Y - I||_max <= 1e-10 (the next update squares the
         // error below double rounding), at most 60 times; the final
         // iteration skips the Y update nobody reads
-        double acc[2][4][2];
         for (int it = 0; finite && it < 60; ++it) {
             // T = 3I - Z Y, with the residual max |T - 2I| = max |Z Y - I|
-            double res = 0.0;
-            if (gw) {
-                warp_gemm(Z, Y, mp, ld, br, bc, lane, acc);
-                warp_store(T, mp, ld, br, bc, lane, acc, -1.0, 3.0);
-#pragma unroll
-                for (int r = 0; r < 2; ++r)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-#pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const int row = 8 * (2 * br + r) + (lane >> 2);
-                            const int col = 8 * (4 * bc + q) + 2 * (lane & 3) + e;
-                            if (row < mp && col < mp)
-                                res = fmax(res, fabs(acc[r][q][e] - (row == col ? 1.0 : 0.0)));
-                        }
-            }
+            g.compute(Z, Y, ld, lane);
+            double res = g.store(T, ld, lane, -1.0, 3.0);
             for (int o = 16; o; o >>= 1) res = fmax(res, __shfl_xor_sync(0xffffffffu, res, o));
             if (lane == 0) red[warp] = res;
             __syncthreads();
@@ -627,14 +632,14 @@ __global__ void __launch_bounds__(256) letkf_point_ns_kernel(PointArgs a) {
             const bool last = !(res > 1e-10);  // (fmax drops NaN: caught below)
             if (!last) {
                 // Y <- Y T / 2 (in place once every warp has read Y)
-                if (gw) warp_gemm(Y, T, mp, ld, br, bc, lane, acc);
+                g.compute(Y, T, ld, lane);
                 __syncthreads();
-                if (gw) warp_store(Y, mp, ld, br, bc, lane, acc, 0.5, 0.0);
+                g.store(Y, ld, lane, 0.5, 0.0);
             }
             // Z <- T Z / 2
-            if (gw) warp_gemm(T, Z, mp, ld, br, bc, lane, acc);
+            g.compute(T, Z, ld, lane);
             __syncthreads();
-            if (gw) warp_store(Z, mp, ld, br, bc, lane, acc, 0.5, 0.0);
+            g.store(Z, ld, lane, 0.5, 0.0);
             __syncthreads();
             if (last) break;
         }
@@ -666,10 +671,13 @@ __global__ void __launch_bounds__(256) letkf_point_ns_kernel(PointArgs a) {
         // both levels with the same transform (proj/src/letkf.cpp:162-171)
         for (int lev = 0; lev < 2; ++lev) {
             const int64_t row = lev ? row1 : row0;
+            for (int j = tid; j < m; j += nt) u[j] = a.x[size_t(j) * a.d + row];
+            __syncthreads();
+            // ensemble_mean: member-order sum times 1/m (proj/src/ensemble.cpp:7-16)
             double mean = 0.0;
-            for (int j = 0; j < m; ++j) mean += a.x[size_t(j) * a.d + row];
+            for (int j = 0; j < m; ++j) mean += u[j];
             mean *= 1.0 / double(m);
-            for (int j = tid; j < m; j += nt) pert[j] = a.x[size_t(j) * a.d + row] - mean;
+            for (int j = tid; j < m; j += nt) pert[j] = u[j] - mean;
             __syncthreads();
             double wx = 0.0;
             for (int k = 0; k < m; ++k) wx += pert[k] * wbar[k];
@@ -1041,13 +1049,23 @@ int turbda_letkf_analyze(const turbda_letkf_params* p, const double* forecast, c
             pn.x = dx;
             pn.out = dout;
             pn.singular = w->singular.as<unsigned long long>();
-            LK_CUDA(cudaFuncSetAttribute(letkf_point_ns_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_ns)));
+            void (*kern)(PointArgs) = nullptr;
+            switch (mp / 8) {
+                case 1: kern = letkf_point_ns_kernel<1>; break;
+                case 2: kern = letkf_point_ns_kernel<2>; break;
+                case 3: kern = letkf_point_ns_kernel<3>; break;
+                case 4: kern = letkf_point_ns_kernel<4>; break;
+                case 5: kern = letkf_point_ns_kernel<5>; break;
+                case 6: kern = letkf_point_ns_kernel<6>; break;
+                case 7: kern = letkf_point_ns_kernel<7>; break;
+                default: kern = letkf_point_ns_kernel<8>; break;
+            }
+            LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem_ns)));
             int per_sm_ns = 0;
-            LK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_ns, letkf_point_ns_kernel,
-                                                                  256, smem_ns));
+            LK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_ns, kern, 256, smem_ns));
             const int64_t grid_ns = std::min<int64_t>(P, int64_t(std::max(per_sm_ns, 1)) * nsm);
-            letkf_point_ns_kernel<<<unsigned(grid_ns), 256, smem_ns, s>>>(pn);
+            kern<<<unsigned(grid_ns), 256, smem_ns, s>>>(pn);
             LK_CUDA(cudaGetLastError());
             add_launches(1);
         } else {

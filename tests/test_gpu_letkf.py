@@ -150,3 +150,18 @@ def test_letkf_device_pointers_and_uniform_r(capi):
                    stream=torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), host)
+
+
+@pytest.mark.parametrize("r,tol", [(1e-2, 1e-10), (1e-4, 1e-9), (1e-6, 1e-7)])
+def test_letkf_ill_conditioned_local_problems(capi, r, tol):
+    """Accurate observations make A = (M-1) I + Yb^T R^-1 Yb ill-conditioned
+    (condition ~ 1/r): the tensor-core Newton-Schulz transform must still
+    converge and agree with the eigendecomposition of the restatement (the
+    tolerance follows the conditioning of W = sqrt(M-1) A^-1/2)."""
+    n, m = 16, 20
+    d = 2 * n * n
+    x = ens(m, d, 31)
+    y = np.random.default_rng(4).standard_normal(d)
+    got = capi.letkf_analyze(x, y, r, nx=n, ny=n, cutoff_km=1500.0)
+    want = L.letkf_analyze(x, y, r, None, n, n, cutoff_km=1500.0)
+    assert rel_err(got, want) < tol
