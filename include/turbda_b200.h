@@ -23,6 +23,9 @@
  *   turbda_rtps_inflate   <- turbda::rtps_inflate     include/turbda/letkf.hpp:54-56,
  *                                                    src/letkf.cpp:177-207
  *   turbda_gaspari_cohn   <- turbda::gaspari_cohn     src/letkf.cpp:10-18
+ *   turbda_snapshot_*     <- turbda::write_snapshot / read_snapshot
+ *                                                    include/turbda/snapshot.hpp:12-23,
+ *                                                    src/snapshot.cpp:12-63
  *
  * Error convention: every entry point returns a turbda_code and fills
  * *status (when non-NULL).  The C++ host maps TURBDA_CONFIG -> ConfigError,
@@ -60,8 +63,9 @@ typedef enum turbda_code {
     TURBDA_INTERNAL = 6,
     TURBDA_BLOWUP = 7,     /* BlowupError(time, member): SQG state non-finite */
     TURBDA_ABORTED = 8,    /* RunAbortedError(cycle): status.diverged_step  */
-    TURBDA_SINGULAR = 9    /* SingularAnalysisError(ix, iy): LETKF, grid point */
+    TURBDA_SINGULAR = 9,   /* SingularAnalysisError(ix, iy): LETKF, grid point */
                            /* in status.diverged_particle / diverged_step    */
+    TURBDA_IO = 10         /* IoError (snapshot files)                      */
 } turbda_code;
 
 typedef enum turbda_precision {
@@ -300,6 +304,18 @@ TURBDA_API int turbda_rtps_inflate(const double* analysis, const double* backgro
                                    uint32_t flags, void* stream, turbda_status* status);
 /* Gaspari-Cohn correlation at normalized distance r (TURBDA_CONFIG for r < 0) */
 TURBDA_API int turbda_gaspari_cohn(double r, double* out, turbda_status* status);
+
+/* SQGSNAP v1 snapshot / ensemble checkpoint files (write_snapshot /
+ * read_snapshot, proj/src/snapshot.cpp:12-63): `count` consecutive
+ * [2][ny][nx] fp64 states, one header each; host or device buffers
+ * (TURBDA_INPUTS_ON_DEVICE).  read: up to max_count snapshots; states NULL
+ * only queries count / nx / ny / time. */
+TURBDA_API int turbda_snapshot_write(const char* path, const double* states, int32_t count,
+                                     int32_t nx, int32_t ny, double time_hours, uint32_t flags,
+                                     turbda_status* status);
+TURBDA_API int turbda_snapshot_read(const char* path, double* states, int32_t max_count,
+                                    int32_t* count, int32_t* nx, int32_t* ny, double* time_hours,
+                                    uint32_t flags, turbda_status* status);
 
 /* Number of CUDA devices (0 when none), library ABI version, and the name of
  * the kernel family compiled in ("sm_100a"). */

@@ -378,6 +378,27 @@ class RefCycleOracle:
                                          C.c_int64, C.c_double, C.c_double, C.c_double, C.c_int,
                                          _dp, C.c_char_p, C.c_int]
 
+    def snapshot_write(self, path, state, nx, ny, time_hours):
+        """the reference's own write_snapshot (proj/src/snapshot.cpp)"""
+        s = np.ascontiguousarray(state, np.float64).ravel()
+        msg = C.create_string_buffer(512)
+        self.lib.refc_snapshot_write.argtypes = [C.c_char_p, _dp, C.c_int, C.c_int, C.c_double,
+                                                 C.c_char_p, C.c_int]
+        if self.lib.refc_snapshot_write(str(path).encode(), s, nx, ny, time_hours, msg, 512):
+            raise OracleError(5, msg.value.decode())
+
+    def snapshot_read(self, path, max_n=1 << 24):
+        out = np.empty(max_n, np.float64)
+        n, nx, ny, t = C.c_long(), C.c_int(), C.c_int(), C.c_double()
+        msg = C.create_string_buffer(512)
+        self.lib.refc_snapshot_read.argtypes = [C.c_char_p, _dp, C.c_long, C.POINTER(C.c_long),
+                                                C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                                C.POINTER(C.c_double), C.c_char_p, C.c_int]
+        if self.lib.refc_snapshot_read(str(path).encode(), out, max_n, C.byref(n), C.byref(nx),
+                                       C.byref(ny), C.byref(t), msg, 512):
+            raise OracleError(5, msg.value.decode())
+        return out[: n.value].reshape(2, ny.value, nx.value), t.value
+
     def letkf_analyze(self, x, y, r, idx, nx, ny, cutoff_km=2000.0, domain_km=20000.0,
                       rtps_alpha=0.3, workers=0):
         """The C++ LETKF restatement (oracle/letkf_restated.cpp) through the

@@ -6,6 +6,8 @@
 //                          (JSON config: turbda::config_from_json, proj/src/config.cpp:64-131)
 //   refc_sqg_advance    -> turbda::SqgStepper::advance proj/src/forecast.cpp:14-32
 //   refc_nature_run     -> turbda::nature_run      proj/src/osse.cpp:101-135
+//   refc_snapshot_write -> turbda::write_snapshot  proj/src/snapshot.cpp:12-30
+//   refc_snapshot_read  -> turbda::read_snapshot   proj/src/snapshot.cpp:32-63
 //   refc_letkf_analyze  -> turbda::letkf_analyze   (restated without Eigen,
 //                          oracle/letkf_restated.cpp; the cycle driver's
 //                          "letkf" variant calls the same function)
@@ -20,6 +22,7 @@
 #include "turbda/config.hpp"
 #include "turbda/forecast.hpp"
 #include "turbda/osse.hpp"
+#include "turbda/snapshot.hpp"
 
 
 using namespace turbda;
@@ -102,6 +105,39 @@ int refc_nature_run(int nx, int ny, double lx, double ly, double h, double spinu
             ++n;
         }
         *n_snaps = n;
+        return 0;
+    } catch (const std::exception& e) {
+        put(msg, msglen, e.what());
+        return 1;
+    }
+}
+
+int refc_snapshot_write(const char* path, const double* state, int nx, int ny, double time_hours,
+                        char* msg, int msglen) {
+    try {
+        GridSpec g;
+        g.nx = nx;
+        g.ny = ny;
+        write_snapshot(std::string(path), PhysicalField(g, std::vector<double>(state, state + g.grid_size())),
+                       time_hours);
+        return 0;
+    } catch (const std::exception& e) {
+        put(msg, msglen, e.what());
+        return 1;
+    }
+}
+
+// out: at least max_n doubles; *n = values read
+int refc_snapshot_read(const char* path, double* out, long max_n, long* n, int* nx, int* ny,
+                       double* time_hours, char* msg, int msglen) {
+    try {
+        const Snapshot s = read_snapshot(std::string(path));
+        *nx = s.field.grid.nx;
+        *ny = s.field.grid.ny;
+        *time_hours = s.time_hours;
+        *n = long(s.field.data.size());
+        if (*n > max_n) throw IoError("buffer too small");
+        std::memcpy(out, s.field.data.data(), sizeof(double) * s.field.data.size());
         return 0;
     } catch (const std::exception& e) {
         put(msg, msglen, e.what());

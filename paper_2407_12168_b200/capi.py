@@ -16,7 +16,7 @@ import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libturbda_b200.so"
 
-OK, CONFIG, DIMENSION, DIVERGED, DOMAIN, CUDA, INTERNAL, BLOWUP, ABORTED, SINGULAR = range(10)
+OK, CONFIG, DIMENSION, DIVERGED, DOMAIN, CUDA, INTERNAL, BLOWUP, ABORTED, SINGULAR, IO = range(11)
 VARIANT_FREE_RUN, VARIANT_LETKF, VARIANT_ENSF = 0, 1, 2
 SCORE_COMPONENTWISE, SCORE_JOINT = 0, 1
 FP32, FP64 = 0, 1
@@ -155,6 +155,13 @@ def lib() -> C.CDLL:
         L.turbda_rtps_inflate.restype = C.c_int
         L.turbda_gaspari_cohn.argtypes = [C.c_double, dp, C.POINTER(Status)]
         L.turbda_gaspari_cohn.restype = C.c_int
+        L.turbda_snapshot_write.argtypes = [C.c_char_p, vp, C.c_int32, C.c_int32, C.c_int32,
+                                            C.c_double, C.c_uint32, C.POINTER(Status)]
+        L.turbda_snapshot_write.restype = C.c_int
+        L.turbda_snapshot_read.argtypes = [C.c_char_p, vp, C.c_int32, C.POINTER(C.c_int32),
+                                           C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                           C.POINTER(C.c_double), C.c_uint32, C.POINTER(Status)]
+        L.turbda_snapshot_read.restype = C.c_int
         _lib = L
     return _lib
 
@@ -290,6 +297,30 @@ def gaspari_cohn(r: float) -> float:
     st = Status()
     _check(lib().turbda_gaspari_cohn(r, C.byref(v), C.byref(st)), st)
     return v.value
+
+
+def snapshot_write(path, states, time_hours=0.0, flags=0):
+    """SQGSNAP v1: `states` (..., 2, ny, nx) float64 (numpy, or a CUDA tensor
+    with flags=INPUTS_ON_DEVICE), one snapshot per leading index."""
+    shape = tuple(states.shape)
+    ny, nx = shape[-2], shape[-1]
+    count = int(np.prod(shape[:-3])) if len(shape) > 3 else 1
+    a = states if flags & INPUTS_ON_DEVICE else np.ascontiguousarray(states, np.float64)
+    st = Status()
+    _check(lib().turbda_snapshot_write(str(path).encode(), _ptr(a), count, nx, ny, time_hours,
+                                       flags, C.byref(st)), st)
+
+
+def snapshot_read(path, max_count=1 << 20):
+    """-> (states [count, 2, ny, nx], time_hours)"""
+    n, nx, ny, t = C.c_int32(), C.c_int32(), C.c_int32(), C.c_double()
+    st = Status()
+    _check(lib().turbda_snapshot_read(str(path).encode(), None, max_count, C.byref(n), C.byref(nx),
+                                      C.byref(ny), C.byref(t), 0, C.byref(st)), st)
+    out = np.empty((n.value, 2, ny.value, nx.value), np.float64)
+    _check(lib().turbda_snapshot_read(str(path).encode(), _ptr(out), n.value, C.byref(n),
+                                      C.byref(nx), C.byref(ny), C.byref(t), 0, C.byref(st)), st)
+    return out, t.value
 
 
 def _status_msg(msg: str) -> Status:

@@ -34,6 +34,7 @@ namespace {
         case TURBDA_DIVERGED: throw SamplerDivergedError(st.diverged_t);
         case TURBDA_DOMAIN: throw std::domain_error(st.msg);
         case TURBDA_SINGULAR: throw SingularAnalysisError(st.diverged_particle, st.diverged_step);
+        case TURBDA_IO: throw IoError(st.msg);
         default: throw std::runtime_error(std::string("turbda_b200: ") + st.msg);
     }
 }

@@ -1,9 +1,10 @@
-"""The reference's own hot-path unit tests (proj/tests/test_{ensf,rng,
-ensemble,parallel}.cpp, 38 cases), compiled unmodified against
+"""The reference's own unit tests for the path (proj/tests/test_{ensf,rng,
+ensemble,parallel,snapshot}.cpp, 42 cases), compiled unmodified against
 include/turbda/*.hpp and linked to libturbda_b200.so (oracle/reftests) -
 the drop-in check for the C++ API.
 
-Against its own implementation the reference passes 35 of the 38; the 3
+Against its own implementation the reference passes 35 of the 38 hot-path
+cases (the 4 snapshot cases pass everywhere); the 3
 failures are defects of the tests: a Philox KAT typo
 (test_rng.cpp:23), a sign error in the shrinkage test (test_ensf.cpp:189-199)
 and the bimodal crossing test, which the reference's Euler-Maruyama misses at
@@ -38,7 +39,8 @@ def test_host_only_reference_cases():
     """RNG, parallel_for and the operator/ensemble cases need no GPU."""
     for filt in ("philox", "splitmix", "stream", "uniform", "normal moments", "distinct",
                  "parallel_for", "TURBDA_WORKERS", "grid operators", "adjoint",
-                 "operator locations", "observation validation", "ensemble validation"):
+                 "operator locations", "observation validation", "ensemble validation",
+                 "snapshot"):
         passed, failed, out = _run(filt)
         assert passed | failed, filt
         assert failed <= EXPECTED_FAILURES, out
@@ -48,7 +50,7 @@ def test_host_only_reference_cases():
 def test_reference_suite_on_b200():
     passed, failed, out = _run()
     print(out[-3000:])
-    assert len(passed) + len(failed) == 38
+    assert len(passed) + len(failed) == 42
     assert failed == EXPECTED_FAILURES, out
 
 
