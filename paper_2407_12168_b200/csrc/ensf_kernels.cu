@@ -649,13 +649,23 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
     const int variant = f32_variant();
     const size_t smem = sizeof(StepF32) * size_t(a.n_steps) +
                         (global_x ? 0 : sizeof(float2) * 32 * size_t(a.m));
-    // 3 CTAs of 256 threads per SM (<= 85 registers): measured best; letting
-    // ptxas take more registers (1 CTA/SM) loses ~20%
+    // letting ptxas take more registers (1 CTA/SM) loses ~20%
+    // register budget: the sorted kernel (N > 24) runs best at 80 registers
+    // (3 CTAs of 256 threads per SM), the brute-force-shift kernel (N <= 24,
+    // fewer warps per CTA) at 64 (measured, tools/sweep_ctas.sh: config 3
+    // -2.7 %); TURBDA_F32_CTAS=3|4 overrides for experiments
+    static const int ctas_env = [] {
+        const char* e = std::getenv("TURBDA_F32_CTAS");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int ctas = ctas_env ? ctas_env : (sorted ? 3 : 4);
     auto kern = global_x ? (a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3, true>
                                         : ensf_f32_kernel<P, false, false, 0, 3, true>)
                 : a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3>
-                : !sorted   ? ensf_f32_kernel<P, false, false, 0, 3>
+                : !sorted   ? (ctas == 4 ? ensf_f32_kernel<P, false, false, 0, 4>
+                                         : ensf_f32_kernel<P, false, false, 0, 3>)
                 : variant == 1 ? ensf_f32_kernel<P, false, true, 8, 3>
+                : ctas == 4    ? ensf_f32_kernel<P, false, true, 0, 4>
                                : ensf_f32_kernel<P, false, true, 0, 3>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
