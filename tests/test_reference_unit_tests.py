@@ -1,5 +1,6 @@
-"""The reference's own unit tests for the path (proj/tests/test_{ensf,rng,
-ensemble,parallel,snapshot}.cpp, 42 cases), compiled unmodified against
+"""The reference's own unit tests for the path and the widened rows
+(proj/tests/test_{ensf,rng,ensemble,parallel,snapshot,forecast,osse}.cpp,
+65 cases), compiled unmodified against
 include/turbda/*.hpp and linked to libturbda_b200.so (oracle/reftests) -
 the drop-in check for the C++ API.
 
@@ -18,17 +19,23 @@ import pytest
 from conftest import ROOT
 
 BIN = ROOT / "oracle" / "_ref" / "reftests_b200"
+REF_BIN = ROOT / "oracle" / "_ref" / "reftests_ref"  # the same files against the reference
 EXPECTED_FAILURES = {
     "philox4x32 known-answer vectors",
     "reverse SDE step: zero scores and zero noise shrink toward origin",
     "analyze pulls a collapsed prior toward a bimodal-side observation",
+    # the reference throws DimensionError where its test expects ConfigError
+    "climatological amplitude is the RMS over the trajectory",
+    # the reference's own EnSF misses this property on the tiny test config
+    # (measured: reftests_ref fails it at the same checks)
+    "assimilation beats the free run on its own forecasts",
 }
 
 
-def _run(filt=None):
-    if not BIN.exists():
-        pytest.skip("oracle/_ref/reftests_b200 not built (needs /root/reference at build time)")
-    cmd = [str(BIN)] + ([filt] if filt else [])
+def _run(filt=None, binary=BIN):
+    if not binary.exists():
+        pytest.skip(f"{binary} not built (needs /root/reference at build time)")
+    cmd = [str(binary)] + ([filt] if filt else [])
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600).stdout
     failed = set(re.findall(r"^\[FAIL\] (.*) \(", out, re.M))
     passed = set(re.findall(r"^\[PASS\] (.*) \(", out, re.M))
@@ -37,10 +44,12 @@ def _run(filt=None):
 
 def test_host_only_reference_cases():
     """RNG, parallel_for and the operator/ensemble cases need no GPU."""
-    for filt in ("philox", "splitmix", "stream", "uniform", "normal moments", "distinct",
+    for filt in ("philox", "splitmix", "stream", "uniform", "normal moments", "distinct entities",
                  "parallel_for", "TURBDA_WORKERS", "grid operators", "adjoint",
                  "operator locations", "observation validation", "ensemble validation",
-                 "snapshot"):
+                 "snapshot round", "snapshot header", "corrupt", "snapshot file", "config json",
+                 "partial configs", "config hash", "experiment config", "model error config",
+                 "metrics serialization"):
         passed, failed, out = _run(filt)
         assert passed | failed, filt
         assert failed <= EXPECTED_FAILURES, out
