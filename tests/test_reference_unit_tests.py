@@ -59,8 +59,18 @@ def test_host_only_reference_cases():
 def test_reference_suite_on_b200():
     passed, failed, out = _run()
     print(out[-3000:])
-    assert len(passed) + len(failed) == 42
+    assert len(passed) + len(failed) == 65
     assert failed == EXPECTED_FAILURES, out
+
+
+@pytest.mark.gpu
+def test_reference_suite_same_verdicts_as_reference():
+    """The same 65 cases linked against the reference implementation (the
+    cycle oracle, cuFFTW build) fail exactly where the B200 build fails."""
+    passed_r, failed_r, out_r = _run(binary=REF_BIN)
+    passed, failed, _ = _run()
+    assert failed_r == failed, out_r
+    assert passed_r == passed
 
 
 CPP_LETKF = ROOT / "tests" / "cpp" / "_build" / "test_cpp_letkf"
