@@ -19,7 +19,9 @@
 //                  Maruyama update with the particle noise, in place
 // Every step streams Z and X through HBM (40 N d bytes at N = J): this mode
 // is HBM / FP64-bound, not SFU-bound.
+#include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 #include <climits>
 #include <cstdint>
 
@@ -304,6 +306,150 @@ __global__ void __launch_bounds__(kJW * 32, 2) joint_apply_kernel(
     }
 }
 
+// Tensor-core form of joint_apply for N <= 64: per 64-coordinate tile the
+// weighted prior sums xbar = W X_tile are ONE 64 x 64 x 64 fp64 GEMM on the
+// FP64 tensor cores (DMMA.8x8x4, W and the member tile staged in shared
+// memory), and the accumulator layout hands each thread a (particle,
+// coordinate pair) — exactly the unit of the Euler-Maruyama update and of
+// one Philox block of particle noise — so the update runs in the epilogue.
+// Persistent CTAs keep W resident and stream X tiles; X is read once per step.
+constexpr int kTcLdx = 72;  // X tile row stride (doubles): conflict-free B loads
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+template <bool kF32Noise>
+__global__ void __launch_bounds__(256) joint_apply_tc_kernel(
+    KernelArgs a, const double* __restrict__ x, const double2* __restrict__ ab,
+    const double* __restrict__ wn, StepF64 c, int step, double* __restrict__ z,
+    unsigned long long* __restrict__ status, int64_t ntiles) {
+    extern __shared__ double jsm[];
+    const int m = a.m;
+    const int mp8 = (m + 7) & ~7;  // particle rows, 8 per warp
+    const int mk = (m + 3) & ~3;   // members: the GEMM's K, 4 per DMMA
+    const int ldw = mk + 4;
+    double* Ws = jsm;                                 // [mp8][ldw]
+    double* const X0 = jsm + size_t(mp8) * ldw;      // [2][mk][kTcLdx] (double buffer)
+    const size_t xsz = size_t(mk) * kTcLdx;
+    double2* const AB0 = reinterpret_cast<double2*>(X0 + 2 * xsz);  // [2][64] {A, B}
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int lr = lane >> 2, lk = lane & 3;
+    const bool aligned = (a.dl & 1) == 0;
+
+    // X tile -> shared memory with cp.async (16 B per copy), zero padding
+    const auto issue = [&](int64_t tile, double* Xs, double2* abs) {
+        const int64_t k0 = tile * 64;
+        for (int q = tid; q < 64; q += nt) {
+            if (k0 + q < a.dl) cp_async16(abs + q, ab + k0 + q);
+            else abs[q] = make_double2(0.0, 0.0);
+        }
+        for (int q = tid; q < mk * 32; q += nt) {
+            const int j = q >> 5, l = q & 31;
+            const int64_t k = k0 + 2 * l;
+            double* dst = Xs + j * kTcLdx + 2 * l;
+            const double* row = x + size_t(j) * size_t(a.dl);
+            if (j < m && aligned && k + 1 < a.dl) {
+                cp_async16(dst, row + k);
+            } else {
+                dst[0] = (j < m && k < a.dl) ? __ldg(row + k) : 0.0;
+                dst[1] = (j < m && k + 1 < a.dl) ? __ldg(row + k + 1) : 0.0;
+            }
+        }
+        cp_async_commit();
+    };
+
+    for (int r = warp; r < mp8; r += nt >> 5)
+        for (int j = lane; j < mk; j += 32)
+            Ws[r * ldw + j] = (r < m && j < m) ? wn[size_t(r) * m + j] : 0.0;
+    const int i = 8 * warp + lr;  // this thread's particle
+    const double ib2 = 2.0 * c.inv2b;
+    int buf = 0;
+    if (int64_t(blockIdx.x) < ntiles) issue(blockIdx.x, X0, AB0);
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
+        const int64_t k0 = tile * 64;
+        const int64_t next = tile + gridDim.x;
+        if (next < ntiles) {
+            issue(next, X0 + (buf ^ 1) * xsz, AB0 + (buf ^ 1) * 64);  // released by the last barrier
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();  // this tile's X (and W) visible to every warp
+        const double* Xs = X0 + buf * xsz;
+        const double2* abs = AB0 + buf * 64;
+        if (8 * warp < mp8) {
+            double acc[8][2];
+#pragma unroll
+            for (int n8 = 0; n8 < 8; ++n8) acc[n8][0] = acc[n8][1] = 0.0;
+            for (int kq = 0; kq < mk; kq += 4) {
+                const double av = Ws[(8 * warp + lr) * ldw + kq + lk];
+                const double* xb = Xs + (kq + lk) * kTcLdx + lr;
+#pragma unroll
+                for (int n8 = 0; n8 < 8; ++n8) dmma_8x8x4(acc[n8], av, xb[8 * n8]);
+            }
+            // epilogue: particle i, coordinates k0 + 8 n8 + 2 lk + {0, 1}; the
+            // particle's z pairs are loaded up front so their latencies overlap
+            if (i < m) {
+                double* zrow = z + size_t(i) * size_t(a.dl);
+                double2 zp[8];
+#pragma unroll
+                for (int n8 = 0; n8 < 8; ++n8) {
+                    const int64_t kl = k0 + 8 * n8 + 2 * lk;
+                    zp[n8] = make_double2(0.0, 0.0);
+                    if (aligned && kl + 1 < a.dl)
+                        zp[n8] = *reinterpret_cast<const double2*>(zrow + kl);
+                    else if (kl < a.dl)
+                        zp[n8] = make_double2(zrow[kl], kl + 1 < a.dl ? zrow[kl + 1] : 0.0);
+                }
+#pragma unroll
+                for (int n8 = 0; n8 < 8; ++n8) {
+                    const int64_t kl = k0 + 8 * n8 + 2 * lk;
+                    if (kl >= a.dl) continue;
+                    const bool has_y = kl + 1 < a.dl;
+                    const double2 o0 = abs[8 * n8 + 2 * lk];
+                    const double2 o1 = abs[8 * n8 + 2 * lk + 1];
+                    double zx = zp[n8].x, zy = zp[n8].y;
+                    double scx = -(zx - c.alpha * acc[n8][0]) * ib2;
+                    double scy = -(zy - c.alpha * acc[n8][1]) * ib2;
+                    if (a.obs_atan) {
+                        scx += c.damp * ((o0.y - o0.x * atan(zx)) / (1.0 + zx * zx));
+                        scy += c.damp * ((o1.y - o1.x * atan(zy)) / (1.0 + zy * zy));
+                    } else {
+                        scx += c.damp * (o0.y - o0.x * zx);
+                        scy += c.damp * (o1.y - o1.x * zy);
+                    }
+                    const uint64_t n0 =
+                        uint64_t(step + 1) * uint64_t(a.d_total) + uint64_t(a.k0 + kl);
+                    double2 xi;
+                    if (kF32Noise) {
+                        const float2 f = normal_pair_f32(n0, uint32_t(i), a.cycle_lo, a.key0, a.key1);
+                        xi = make_double2(f.x, f.y);
+                    } else {
+                        xi = normal_pair_f64(n0, uint32_t(i), a.cycle_lo, a.key0, a.key1);
+                    }
+                    zx += -(c.b * zx - c.s2 * scx) * c.dt + c.sig * xi.x;
+                    zy += -(c.b * zy - c.s2 * scy) * c.dt + c.sig * xi.y;
+                    if (aligned && has_y) {
+                        *reinterpret_cast<double2*>(zrow + kl) = make_double2(zx, zy);
+                    } else {
+                        zrow[kl] = zx;
+                        if (has_y) zrow[kl + 1] = zy;
+                    }
+                    if (!isfinite(zx) || (has_y && !isfinite(zy)))
+                        atomicMin(status, (uint64_t(i) << 32) | uint32_t(step));
+                }
+            }
+        }
+        __syncthreads();  // every warp is done with this X buffer
+    }
+}
+
 }  // namespace
 
 JointPlan joint_plan(int n, int m, int64_t dl) {
@@ -356,6 +502,31 @@ cudaError_t launch_joint_update(const KernelArgs& a, const double* x, const doub
                                                                   wn);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || a.dl <= 0) return e;
+    static const int tc_env = [] {
+        const char* e = std::getenv("TURBDA_JOINT_TC");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (a.m <= 64 && tc_env) {
+        const int mp8 = (a.m + 7) & ~7, mk = (a.m + 3) & ~3;
+        const size_t smem = sizeof(double) * (size_t(mp8) * (mk + 4) + 2 * size_t(mk) * kTcLdx + 256);
+        const int threads = 32 * (mp8 / 8);
+        auto kern = f32_noise ? joint_apply_tc_kernel<true> : joint_apply_tc_kernel<false>;
+        static int per_sm[2] = {0, 0};
+        int& ps = per_sm[f32_noise ? 1 : 0];
+        if (smem > 48 * 1024) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            if (e != cudaSuccess) return e;
+        }
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, threads, smem);
+        if (e != cudaSuccess) return e;
+        const int64_t ntiles = (a.dl + 63) / 64;
+        const int64_t grid = std::min<int64_t>(ntiles, int64_t(std::max(ps, 1)) * nsm);
+        kern<<<unsigned(grid), threads, smem, st>>>(a, x, ab, wn, c, step, z, status, ntiles);
+        return cudaGetLastError();
+    }
     const dim3 grid(unsigned((a.dl + 63) / 64), unsigned((a.m + kJP * kJW - 1) / (kJP * kJW)));
     if (f32_noise)
         joint_apply_kernel<true><<<grid, kJW * 32, 0, st>>>(a, x, ab, wn, c, step, z, status);
