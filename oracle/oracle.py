@@ -451,3 +451,41 @@ class RefCycleOracle:
         if code:
             raise OracleError(5, msg.value.decode())
         return out.reshape(n_snap, 2 * nx * ny)[: n.value]
+
+
+class RefPython:
+    """The reference's own Python binding (proj/python/bindings.cpp) built by
+    ``make -C oracle refpy`` into oracle/_ref/refpy.  pybind11 would clash on
+    the shared C++ type names (GridSpec, ...) if both bindings lived in one
+    interpreter, so every call runs in a fresh subprocess: ``snippet`` sees
+    the module as ``ref``, numpy as ``np``, the keyword arrays by name, and
+    assigns its results (arrays or JSON-able values) into the dict ``out``."""
+
+    def __init__(self):
+        import glob
+        hits = glob.glob(str(HERE / "_ref" / "refpy" / "_core*.so"))
+        if not hits:
+            raise FileNotFoundError("oracle/_ref/refpy not built (make -C oracle refpy)")
+        self.path = hits[0]
+
+    def run(self, snippet: str, timeout: float = 900, **arrays):
+        import json
+        import pickle
+        import subprocess
+        import sys
+        import tempfile
+        with tempfile.TemporaryDirectory() as tmp:
+            inp, outp = Path(tmp) / "in.pkl", Path(tmp) / "out.pkl"
+            inp.write_bytes(pickle.dumps(arrays))
+            prog = (
+                "import importlib.util, pickle, numpy as np\n"
+                f"spec = importlib.util.spec_from_file_location('refpy._core', {self.path!r})\n"
+                "ref = importlib.util.module_from_spec(spec); spec.loader.exec_module(ref)\n"
+                f"globals().update(pickle.loads(open({str(inp)!r}, 'rb').read()))\n"
+                "out = {}\n" + snippet + "\n"
+                f"open({str(outp)!r}, 'wb').write(pickle.dumps(out))\n")
+            r = subprocess.run([sys.executable, "-c", prog], capture_output=True, text=True,
+                               timeout=timeout)
+            if r.returncode:
+                raise OracleError(5, r.stderr[-2000:])
+            return pickle.loads(outp.read_bytes())

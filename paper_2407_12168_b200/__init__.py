@@ -1,16 +1,21 @@
 """B200-native EnSF analysis step (arXiv 2407.12168) behind the turbda API.
 
-Mirrors the reference Python package's EnSF surface
-(proj/python/turbda/__init__.py:1-37): ``ensf_analyze``, ``GridSpec`` and
-the ``ConfigError`` / ``DimensionError`` exceptions (both ``ValueError``
-subclasses; a diverged sampler raises ``RuntimeError`` as in the reference).
+Mirrors the reference Python package (proj/python/turbda/__init__.py:1-37):
+``ensf_analyze``, ``letkf_analyze``, ``GridSpec``, ``SqgParams``,
+``nature_run``, ``advance``, ``run_experiment``, ``default_config_json``,
+``config_hash`` and the ``ConfigError`` / ``DimensionError`` exceptions (both
+``ValueError`` subclasses; a diverged sampler raises ``RuntimeError`` as in
+the reference).  Not part of this build: ``ke_spectrum`` /
+``fit_loglog_slope`` and the ViT budget helpers (not on the analysis path).
 The compute runs in ``lib/libturbda_b200.so`` (sm_100a); importing without
 the built extension fails loudly - there is no CPU fallback.
 """
-from ._core import ConfigError, DimensionError, GridSpec, ensf_analyze  # noqa: F401
+from ._core import (ConfigError, DimensionError, GridSpec, SqgParams, advance,  # noqa: F401
+                    config_hash, default_config_json, ensf_analyze, letkf_analyze, nature_run)
 from ._core import build_arch, device_count, launch_count  # noqa: F401
 from . import capi  # noqa: F401
-from .experiment import default_config_json, run_experiment  # noqa: F401
+from .experiment import run_experiment  # noqa: F401
 
-__all__ = ["ConfigError", "DimensionError", "GridSpec", "ensf_analyze", "capi", "build_arch",
-           "device_count", "launch_count", "run_experiment", "default_config_json"]
+__all__ = ["ConfigError", "DimensionError", "GridSpec", "SqgParams", "advance", "config_hash",
+           "default_config_json", "ensf_analyze", "letkf_analyze", "nature_run", "run_experiment",
+           "capi", "build_arch", "device_count", "launch_count"]

@@ -1,9 +1,13 @@
 // Python module paper_2407_12168_b200._core - the B200 counterpart of the
-// reference binding's EnSF entry point (proj/python/bindings.cpp:140-155,
-// exceptions :223-224).  ensf_analyze keeps the reference signature and
-// defaults; keyword-only extras select the observation thinning, the
-// arithmetic and the devices.  Arrays go straight from numpy to the device
-// through the C-ABI (no vector<vector<double>> round trip).
+// reference binding (proj/python/bindings.cpp): ensf_analyze (:140-155) and
+// letkf_analyze (:157-172) keep the reference signatures and defaults, with
+// keyword-only extras for the observation thinning, the arithmetic and the
+// devices; arrays go straight from numpy to the device through the C-ABI.
+// GridSpec / SqgParams, nature_run / advance (:87-109, the GPU model),
+// default_config_json / config_hash (:196-202) and the exceptions (:223-224)
+// follow the reference.  run_experiment lives in experiment.py (the
+// GPU-resident cycle driver).  Out of scope: ke_spectrum / fit_loglog_slope
+// and the ViT budget helpers.
 #include <pybind11/numpy.h>
 #include <pybind11/pybind11.h>
 
@@ -11,8 +15,11 @@
 #include <string>
 #include <vector>
 
+#include "turbda/config.hpp"
 #include "turbda/errors.hpp"
+#include "turbda/forecast.hpp"
 #include "turbda/grid.hpp"
+#include "turbda/osse.hpp"
 #include "turbda_b200.h"
 
 namespace py = pybind11;
@@ -27,6 +34,7 @@ using darray = py::array_t<double, py::array::c_style | py::array::forcecast>;
         case TURBDA_DIMENSION: throw turbda::DimensionError(st.msg);
         case TURBDA_DIVERGED: throw turbda::SamplerDivergedError(st.diverged_t);
         case TURBDA_DOMAIN: throw std::domain_error(st.msg);
+        case TURBDA_SINGULAR: throw turbda::SingularAnalysisError(st.diverged_particle, st.diverged_step);
         default: throw std::runtime_error(std::string("turbda_b200: ") + st.msg);
     }
 }
@@ -106,6 +114,52 @@ py::array_t<double> ensf_analyze(const darray& members, const turbda::GridSpec& 
     return out;
 }
 
+py::array_t<double> letkf_analyze(const darray& members, const turbda::GridSpec& grid,
+                                  const darray& y, double r, double cutoff_km, double rtps_alpha,
+                                  int /*workers*/, int thinning, int device) {
+    if (members.ndim() != 2) throw turbda::DimensionError("members must be (M, d)");
+    grid.validate();
+    const auto m = members.shape(0), d = members.shape(1);
+    if (int64_t(grid.grid_size()) != d)
+        throw turbda::DimensionError("letkf_analyze: state/grid size mismatch");
+    std::vector<int64_t> idx;
+    if (thinning > 1)
+        for (int64_t k = 0; k < d; k += thinning) idx.push_back(k);
+    const int64_t obs_dim = thinning > 1 ? int64_t(idx.size()) : d;
+    if (y.size() != obs_dim) throw turbda::DimensionError("observation: length mismatch");
+    if (!(r > 0.0)) throw turbda::ConfigError("observation: r_diag > 0");
+    turbda_letkf_params p;
+    turbda_letkf_params_init(&p);
+    p.nx = grid.nx;
+    p.ny = grid.ny;
+    p.n_members = int32_t(m);
+    p.obs_kind = thinning > 1 ? 1 : 0;
+    p.obs_dim = obs_dim;
+    p.cutoff_km = cutoff_km;
+    p.rtps_alpha = rtps_alpha;
+    p.device = device;
+    p.flags = TURBDA_R_UNIFORM;
+    if (grid.nx != grid.ny || grid.lx != grid.ly)
+        throw turbda::ConfigError("letkf_analyze: isotropic metric needs nx == ny");
+    py::array_t<double> out({m, d});
+    turbda_status st{};
+    int rc;
+    {
+        py::gil_scoped_release nogil;
+        rc = turbda_letkf_analyze(&p, members.data(), y.data(), &r,
+                                  idx.empty() ? nullptr : idx.data(), nullptr, out.mutable_data(),
+                                  nullptr, &st);
+    }
+    if (rc) raise(rc, st);
+    return out;
+}
+
+py::array_t<double> field_array(const turbda::GridSpec& g, const std::vector<double>& v) {
+    py::array_t<double> out({g.nz, g.ny, g.nx});
+    std::copy(v.begin(), v.end(), out.mutable_data());
+    return out;
+}
+
 }  // namespace
 
 PYBIND11_MODULE(_core, mod) {
@@ -131,6 +185,60 @@ PYBIND11_MODULE(_core, mod) {
             py::arg("obs_operator") = "linear", py::arg("score_mode") = "componentwise",
             py::arg("out") = py::none(),
             "EnSF analysis of an (M, d) float64 forecast ensemble on the GPU; returns (M, d)");
+
+    py::class_<turbda::SqgParams>(mod, "SqgParams")
+        .def(py::init<>())
+        .def_readwrite("f", &turbda::SqgParams::f)
+        .def_readwrite("n", &turbda::SqgParams::n)
+        .def_readwrite("u0", &turbda::SqgParams::u0)
+        .def_readwrite("hyper_order", &turbda::SqgParams::hyper_order)
+        .def_readwrite("hyper_efold", &turbda::SqgParams::hyper_efold)
+        .def_readwrite("dt", &turbda::SqgParams::dt)
+        .def_readwrite("drag_tau", &turbda::SqgParams::drag_tau)
+        .def("validate", &turbda::SqgParams::validate);
+
+    mod.def(
+        "nature_run",
+        [](const turbda::GridSpec& grid, const turbda::SqgParams& params, double spinup,
+           double duration, double interval, std::uint64_t seed) {
+            std::vector<std::vector<double>> snaps;
+            {
+                py::gil_scoped_release nogil;
+                snaps = turbda::nature_run(grid, params, spinup, duration, interval, seed);
+            }
+            py::list out;
+            for (const auto& s : snaps) out.append(field_array(grid, s));
+            return out;
+        },
+        py::arg("grid"), py::arg("params"), py::arg("spinup"), py::arg("duration"),
+        py::arg("interval"), py::arg("seed"),
+        "clean model run on the GPU; returns a list of (nz, ny, nx) snapshots");
+
+    mod.def(
+        "advance",
+        [](const turbda::GridSpec& grid, const turbda::SqgParams& params, const darray& state,
+           double hours) {
+            std::vector<double> v(state.data(), state.data() + state.size());
+            {
+                py::gil_scoped_release nogil;
+                turbda::SqgStepper stepper(grid, params);
+                stepper.advance(v, hours);
+            }
+            return field_array(grid, v);
+        },
+        py::arg("grid"), py::arg("params"), py::arg("state"), py::arg("hours"));
+
+    mod.def("letkf_analyze", &letkf_analyze, py::arg("members"), py::arg("grid"), py::arg("y"),
+            py::arg("r") = 1.0, py::arg("cutoff_km") = 2000.0, py::arg("rtps_alpha") = 0.3,
+            py::arg("workers") = 0, py::kw_only(), py::arg("thinning") = 0,
+            py::arg("device") = -1,
+            "LETKF analysis of an (M, d) float64 forecast ensemble on the GPU; returns (M, d)");
+
+    mod.def("default_config_json",
+            [] { return turbda::config_to_json(turbda::ExperimentConfig{}).dump(2); });
+    mod.def("config_hash", [](const std::string& config_json) {
+        return turbda::config_hash(turbda::config_from_json(nlohmann::json::parse(config_json)));
+    });
 
     mod.def("device_count", &turbda_device_count);
     mod.def("build_arch", [] { return std::string(turbda_build_arch()); });
