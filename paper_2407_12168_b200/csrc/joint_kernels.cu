@@ -511,8 +511,7 @@ cudaError_t launch_joint_update(const KernelArgs& a, const double* x, const doub
         const size_t smem = sizeof(double) * (size_t(mp8) * (mk + 4) + 2 * size_t(mk) * kTcLdx + 256);
         const int threads = 32 * (mp8 / 8);
         auto kern = f32_noise ? joint_apply_tc_kernel<true> : joint_apply_tc_kernel<false>;
-        static int per_sm[2] = {0, 0};
-        int& ps = per_sm[f32_noise ? 1 : 0];
+        int ps = 0;
         if (smem > 48 * 1024) {
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             if (e != cudaSuccess) return e;
