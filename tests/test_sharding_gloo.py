@@ -83,3 +83,66 @@ def test_bench_shard_observation_indices():
     for k0 in (0, 1000, 2000, 3000):
         _, _, idx = bench.make_inputs(d, 2, stride, k0)
         assert np.array_equal(idx, np.arange(k0, k0 + d)[np.arange(k0, k0 + d) % stride == 0])
+
+
+def _joint_worker(rank, world, port, result):
+    """Joint-norm score (north_star extension) sharded by coordinates: per
+    pseudo-step each rank forms the N x N partial squared distances over its
+    window, ONE all_reduce(sum) makes them global, and the softmax, weighted
+    prior sum, likelihood and Euler-Maruyama update stay local - the data
+    flow of csrc/joint_kernels.cu + the NCCL allreduce, restated in numpy
+    after oracle/ensf_oracle.c (orc_analyze, joint = 1)."""
+    import sys
+    sys.path.insert(0, str(ROOT))
+    from oracle.oracle import PortOracle, throughput_inputs
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    po = PortOracle()
+    d, m, n_steps, seed, cycle, eps, r = 1000, 12, 15, 7, 1, 0.01, 0.8
+    x, y, idx = throughput_inputs(m, d, oracle=po, stride=3)
+    lo, hi = _shard_bounds(d, world, rank)
+    xl = x[:, lo:hi]
+    sel = (idx >= lo) & (idx < hi)
+    il, yl = idx[sel] - lo, y[sel]
+    fexp = np.vectorize(po.fast_exp_nonpos)
+    ent = [(cycle << 32) | i for i in range(m)]
+    z = np.stack([po.stream_normals(seed, 6, ent[i], hi - lo, lo) for i in range(m)])
+    dt = (1.0 - eps) / n_steps
+    for s in range(n_steps):
+        t = max(1.0 - s * dt - dt, eps)
+        alpha, beta2 = 1.0 - t, t
+        b, s2, damp = -1.0 / (1.0 - t), 1.0 + 2.0 * t / (1.0 - t), 1.0 - t
+        diff = z[:, None, :] - alpha * xl[None, :, :]
+        part = torch.from_numpy(np.einsum("ijk,ijk->ij", diff, diff))
+        dist.all_reduce(part)  # the one collective of the step
+        dd = part.numpy()
+        w = fexp((dd.min(axis=1, keepdims=True) - dd) / (2.0 * beta2))
+        num = w @ xl
+        sc = -(z - alpha * num / w.sum(axis=1, keepdims=True)) / beta2
+        np.add.at(sc, (slice(None), il), damp * (yl - z[:, il]) / r)
+        xi = np.stack([po.stream_normals(seed, 6, ent[i], hi - lo, (s + 1) * d + lo)
+                       for i in range(m)])
+        z = z + (-(b * z - s2 * sc) * dt + np.sqrt(s2 * dt) * xi)
+    part_out = po.relax_spread(z, xl, 1.0)
+    parts = [None] * world
+    dist.all_gather_object(parts, (lo, part_out))
+    if rank == 0:
+        whole = po.analyze(x, y, r, idx, n_steps=n_steps, joint=True, workers=2)
+        got = np.concatenate([p for _, p in sorted(parts, key=lambda t: t[0])], axis=1)
+        err = float(np.linalg.norm(got - whole) / np.linalg.norm(whole))
+        result.put(err)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_joint_mode_one_allreduce_per_step():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_joint_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    err = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+    assert err < 1e-9, err
