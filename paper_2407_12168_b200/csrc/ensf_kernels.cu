@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "ensf_device.h"
+#include "bulk_copy.cuh"
 #include "philox.cuh"
 
 namespace tb200 {
@@ -179,13 +180,20 @@ __global__ void __launch_bounds__(256, kMinBlocks) ensf_f32_kernel(KernelArgs a,
     const int64_t kl = tile0 + 2 * lane;  // local coordinate of this lane's pair
     const bool aligned = ((a.dl & 1) == 0);
 
-    for (int q = threadIdx.x; q < a.n_steps; q += blockDim.x) cs[q] = steps[q];
-    if (!kGlobalX) {
-        // the tile's members, fp32, [m][64] (sorted per column when kSorted),
-        // laid out contiguously by prep_tiles_kernel: coalesced 16 B loads
-        const float4* src = reinterpret_cast<const float4*>(xt + size_t(blockIdx.x) * size_t(a.m) * kTile);
-        float4* dst = reinterpret_cast<float4*>(cs + a.n_steps);
-        for (int q = threadIdx.x; q < a.m * (kTile / 4); q += blockDim.x) dst[q] = __ldg(src + q);
+    // the step table and the tile's members (fp32 [m][64], sorted per column
+    // when kSorted, contiguous by prep_tiles_kernel) arrive by two TMA bulk
+    // copies issued by one thread while the others set up their pairs
+    __shared__ uint64_t tile_bar;
+    if (threadIdx.x == 0) mbar_init(&tile_bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t step_bytes = uint32_t(sizeof(StepF32)) * uint32_t(a.n_steps);
+        const uint32_t tile_bytes = kGlobalX ? 0u : uint32_t(sizeof(float)) * uint32_t(a.m) * kTile;
+        mbar_arrive_expect_tx(&tile_bar, step_bytes + tile_bytes);
+        bulk_copy_g2s(cs, steps, step_bytes, &tile_bar);
+        if (!kGlobalX)
+            bulk_copy_g2s(cs + a.n_steps, xt + size_t(blockIdx.x) * size_t(a.m) * kTile,
+                          tile_bytes, &tile_bar);
     }
     // likelihood operator for this pair: B - A z with A = sum 1/r, B = sum y/r
     float2 A2 = f2(0.f), B2 = f2(0.f);
@@ -203,7 +211,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) ensf_f32_kernel(KernelArgs a,
     const bool has_y = kl + 1 < a.dl;  // the pair's second coordinate is real
     int top = 1;
     while (top * 2 <= a.j_batch) top *= 2;
-    __syncthreads();
+    mbar_wait(&tile_bar, 0);  // step table and member tile have landed
 
     const int i0 = (blockIdx.y * nwarps + warp) * P;
     const uint64_t kg = uint64_t(a.k0 + kl);  // global coordinate of the pair's first entry
