@@ -2,7 +2,8 @@
 """EnSF analysis throughput on B200 (BASELINE.json metric: d x N x steps / s).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config cfg2|cfg1|cfg3|cfg4] [--precision fp32|fp64]
+                    [--config cfg2|cfg1|cfg3|cfg4|cfg5] [--precision fp32|fp64]
+                    [--obs linear|arctan]
 
 One "step" is one full EnSF analysis (turbda::analyze: every pseudo-time
 step of the reverse SDE + relax_spread) of one synthetic forecast ensemble.
@@ -45,6 +46,8 @@ CONFIGS = {
     "cfg2": (131072, 64, 100, 4, "BASELINE cfg2: d=131072 (256x256x2), N=64, S=100, every-4th-point obs"),
     "cfg3": (16777216, 20, 100, 1, "BASELINE cfg3: d=16.8M (2048x2048x4), N=20, S=100"),
     "cfg4": (1048576, 512, 100, 1, "BASELINE cfg4: d=1M, N=512, S=100"),
+    "cfg5": (2097152, 128, 100, 4, "BASELINE cfg5 analysis: d=2.1M (1024x1024x2), N=128, S=100, "
+                                   "every-4th-point arctan obs"),
 }
 # algorithmic bytes per unit for a per-step-streaming fp32
 # design (read z, read x, write z) - the HBM roofline the north star names.
@@ -151,10 +154,11 @@ def make_inputs(d, m, stride, k0, seed=1234):
     return x, y, idx
 
 
-def reference_rate(x, y, idx, n_steps, steps, warmup):
-    """The reference's CPU analyze (oracle/_ref) on the given sample."""
+def reference_rate(x, y, idx, n_steps, steps, warmup, arctan=False):
+    """The reference's CPU analyze (oracle/_ref) on the given sample; arctan
+    observations (an extension the reference lacks) use the C restatement."""
     from oracle.oracle import RefOracle, host_cores, ref_available
-    if not ref_available():
+    if arctan or not ref_available():
         from oracle.oracle import PortOracle
         impl, kind = PortOracle(), "port"
     else:
@@ -162,6 +166,8 @@ def reference_rate(x, y, idx, n_steps, steps, warmup):
     cores = host_cores()
     m, d = x.shape
     kw = dict(n_steps=n_steps, seed=7, cycle=1, workers=cores)
+    if arctan:
+        kw["arctan"] = True
     for _ in range(warmup):
         impl.analyze(x, y, 1.0, idx, **kw)
     times = []
@@ -185,22 +191,36 @@ def run_reference_arm(args, cfg, json_out=None):
     if rank != 0:
         return
     d_full, m, s, stride, desc = CONFIGS[cfg]
-    d_sample = min(d_full, args.ref_sample_d)
+    d_sample = _cpu_sample(d_full, m, args.ref_sample_d)
     x, y, idx = make_inputs(d_sample, m, stride, 0)
-    r = reference_rate(x, y, idx, s, args.steps, args.warmup)
+    r = reference_rate(x, y, idx, s, args.steps, args.warmup, arctan=_arctan(args))
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "d_per_gpu": d_full, "members": m, "pseudo_steps": s,
-                   "obs_stride": stride, "sample_d": d_sample},
+                   "obs_stride": stride, "obs_operator": "arctan" if _arctan(args) else "linear",
+                   "sample_d": d_sample},
         "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"],
                          "kind": r["kind"], "sample": r["sample"]},
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), file=json_out or sys.stdout, flush=True)
+
+
+def _cpu_sample(d, m, base):
+    """CPU sample width: `base` coordinates at N = 64, scaled by (64/N)^2 (the
+    CPU cost grows with N^2 per coordinate) so every config's CPU leg takes
+    seconds, a multiple of 64 coordinates."""
+    return max(64, min(d, int(base * (64.0 / m) ** 2) // 64 * 64))
+
+
+def _arctan(args):
+    """h(x) = atan(x) observations: --obs, defaulting to the config's own
+    (BASELINE config 5 observes through arctan)."""
+    return (args.obs or ("arctan" if args.config == "cfg5" else "linear")) == "arctan"
 
 
 def _json_stdout():
@@ -224,6 +244,8 @@ def main():
     ap.add_argument("--score", choices=["componentwise", "joint"], default="componentwise",
                     help="joint: the north-star joint-norm extension (fp64, one NCCL allreduce "
                          "of the N x N distances per pseudo-step across ranks)")
+    ap.add_argument("--obs", choices=["linear", "arctan"], default=None,
+                    help="observation operator (default: arctan for cfg5, linear otherwise)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-d", type=int, default=32768)
     ap.add_argument("--ref-sample-d", type=int, default=8192)
@@ -254,6 +276,7 @@ def main():
     d_total = d * world
     k0 = rank * d
     joint = args.score == "joint"
+    arctan = _arctan(args)
     # joint mode: distances/update in fp64 always; --precision picks the noise
     prec = capi.FP32 if args.precision == "fp32" else capi.FP64
     if joint and world > 1:
@@ -274,7 +297,8 @@ def main():
     out = torch.empty((m, d), dtype=torch.float64, device=dev)
     obs_dim = host_sets[0][1].size
     p = capi.params(d_total=d_total, k0=k0, d_local=d, obs_dim=obs_dim, n_members=m, n_steps=s,
-                    obs_kind=0 if stride <= 1 else 1, precision=prec, device=local,
+                    obs_kind=(0 if stride <= 1 else 1) + (2 if arctan else 0),
+                    precision=prec, device=local,
                     flags=capi.INPUTS_ON_DEVICE | capi.ASYNC,
                     score_mode=capi.SCORE_JOINT if joint else capi.SCORE_COMPONENTWISE)
     stream = torch.cuda.Stream(dev)  # a real stream: the events and kernels share it
@@ -358,14 +382,16 @@ def main():
         if joint and world > 1:
             # a window of the sharded state: the C-ABI with host buffers
             pe = capi.params(d_total=d_total, k0=k0, d_local=d, obs_dim=obs_dim, n_members=m,
-                             n_steps=s, obs_kind=0 if stride <= 1 else 1, precision=prec,
-                             device=local, cycle=1 + q, score_mode=capi.SCORE_JOINT)
+                             n_steps=s, obs_kind=(0 if stride <= 1 else 1) + (2 if arctan else 0),
+                             precision=prec, device=local, cycle=1 + q,
+                             score_mode=capi.SCORE_JOINT)
             capi.analyze(pe, hx, hy_full, np.ones_like(hy_full), host_sets[0][2], hout)
             res = hout
         else:
             res = tb.ensf_analyze(hx, grid, hy_full, r=1.0, seed=7, cycle=1 + q, n_steps=s,
                                   thinning=stride if stride > 1 else 0,
                                   precision=args.precision, device=local,
+                                  obs_operator="arctan" if arctan else "linear",
                                   score_mode=args.score, out=hout)
         if q >= args.warmup:
             e2e_times.append(time.perf_counter() - t0)
@@ -425,6 +451,7 @@ def main():
         "config": {"workload": desc + (" [joint-norm score extension]" if joint else ""),
                    "score": args.score, "d_per_gpu": d, "d_total": d_total, "members": m,
                    "pseudo_steps": s, "obs_stride": stride,
+                   "obs_operator": "arctan" if arctan else "linear",
                    "l2": (f"L2 flushed (512 MB write) before each step, outside its timing; "
                           f"inputs {set_bytes / 1e6:.0f} MB" if flush else
                           f"{n_sets} rotating resident input sets ({set_bytes / 1e6:.0f} MB; "
@@ -440,8 +467,8 @@ def main():
         "clocks": clk,
     }
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        xs, ys, idxs = make_inputs(min(d, args.cpu_sample_d), m, stride, 0)
-        cb = reference_rate(xs, ys, idxs, s, 1, 0)
+        xs, ys, idxs = make_inputs(_cpu_sample(d, m, args.cpu_sample_d), m, stride, 0)
+        cb = reference_rate(xs, ys, idxs, s, 1, 0, arctan=arctan)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(line), file=json_out, flush=True)
