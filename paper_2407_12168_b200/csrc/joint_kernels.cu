@@ -323,6 +323,69 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
+// The update of one particle's 8 coordinate pairs of a 64-coordinate tile
+// from its weighted prior sums `acc` (the DMMA accumulator layout: pair
+// k0 + 8 n8 + 2 lk): score, damped likelihood, particle noise, Euler-
+// Maruyama, divergence check.  The particle's z pairs are loaded up front so
+// their latencies overlap.
+template <bool kF32Noise>
+__device__ __forceinline__ void joint_update_epilogue(const KernelArgs& a, const StepF64& c,
+                                                      int step, int i, int64_t k0, int lk,
+                                                      const double (&acc)[8][2],
+                                                      const double2* abs, double* z,
+                                                      unsigned long long* status) {
+    if (i >= a.m) return;
+    const bool aligned = (a.dl & 1) == 0;
+    const double ib2 = 2.0 * c.inv2b;
+    double* zrow = z + size_t(i) * size_t(a.dl);
+    double2 zp[8];
+#pragma unroll
+    for (int n8 = 0; n8 < 8; ++n8) {
+        const int64_t kl = k0 + 8 * n8 + 2 * lk;
+        zp[n8] = make_double2(0.0, 0.0);
+        if (aligned && kl + 1 < a.dl)
+            zp[n8] = *reinterpret_cast<const double2*>(zrow + kl);
+        else if (kl < a.dl)
+            zp[n8] = make_double2(zrow[kl], kl + 1 < a.dl ? zrow[kl + 1] : 0.0);
+    }
+#pragma unroll
+    for (int n8 = 0; n8 < 8; ++n8) {
+        const int64_t kl = k0 + 8 * n8 + 2 * lk;
+        if (kl >= a.dl) continue;
+        const bool has_y = kl + 1 < a.dl;
+        const double2 o0 = abs[8 * n8 + 2 * lk];
+        const double2 o1 = abs[8 * n8 + 2 * lk + 1];
+        double zx = zp[n8].x, zy = zp[n8].y;
+        double scx = -(zx - c.alpha * acc[n8][0]) * ib2;
+        double scy = -(zy - c.alpha * acc[n8][1]) * ib2;
+        if (a.obs_atan) {
+            scx += c.damp * ((o0.y - o0.x * atan(zx)) / (1.0 + zx * zx));
+            scy += c.damp * ((o1.y - o1.x * atan(zy)) / (1.0 + zy * zy));
+        } else {
+            scx += c.damp * (o0.y - o0.x * zx);
+            scy += c.damp * (o1.y - o1.x * zy);
+        }
+        const uint64_t n0 = uint64_t(step + 1) * uint64_t(a.d_total) + uint64_t(a.k0 + kl);
+        double2 xi;
+        if (kF32Noise) {
+            const float2 f = normal_pair_f32(n0, uint32_t(i), a.cycle_lo, a.key0, a.key1);
+            xi = make_double2(f.x, f.y);
+        } else {
+            xi = normal_pair_f64(n0, uint32_t(i), a.cycle_lo, a.key0, a.key1);
+        }
+        zx += -(c.b * zx - c.s2 * scx) * c.dt + c.sig * xi.x;
+        zy += -(c.b * zy - c.s2 * scy) * c.dt + c.sig * xi.y;
+        if (aligned && has_y) {
+            *reinterpret_cast<double2*>(zrow + kl) = make_double2(zx, zy);
+        } else {
+            zrow[kl] = zx;
+            if (has_y) zrow[kl + 1] = zy;
+        }
+        if (!isfinite(zx) || (has_y && !isfinite(zy)))
+            atomicMin(status, (uint64_t(i) << 32) | uint32_t(step));
+    }
+}
+
 template <bool kF32Noise>
 __global__ void __launch_bounds__(256) joint_apply_tc_kernel(
     KernelArgs a, const double* __restrict__ x, const double2* __restrict__ ab,
@@ -368,7 +431,6 @@ __global__ void __launch_bounds__(256) joint_apply_tc_kernel(
         for (int j = lane; j < mk; j += 32)
             Ws[r * ldw + j] = (r < m && j < m) ? wn[size_t(r) * m + j] : 0.0;
     const int i = 8 * warp + lr;  // this thread's particle
-    const double ib2 = 2.0 * c.inv2b;
     int buf = 0;
     if (int64_t(blockIdx.x) < ntiles) issue(blockIdx.x, X0, AB0);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
@@ -393,60 +455,109 @@ __global__ void __launch_bounds__(256) joint_apply_tc_kernel(
 #pragma unroll
                 for (int n8 = 0; n8 < 8; ++n8) dmma_8x8x4(acc[n8], av, xb[8 * n8]);
             }
-            // epilogue: particle i, coordinates k0 + 8 n8 + 2 lk + {0, 1}; the
-            // particle's z pairs are loaded up front so their latencies overlap
-            if (i < m) {
-                double* zrow = z + size_t(i) * size_t(a.dl);
-                double2 zp[8];
-#pragma unroll
-                for (int n8 = 0; n8 < 8; ++n8) {
-                    const int64_t kl = k0 + 8 * n8 + 2 * lk;
-                    zp[n8] = make_double2(0.0, 0.0);
-                    if (aligned && kl + 1 < a.dl)
-                        zp[n8] = *reinterpret_cast<const double2*>(zrow + kl);
-                    else if (kl < a.dl)
-                        zp[n8] = make_double2(zrow[kl], kl + 1 < a.dl ? zrow[kl + 1] : 0.0);
-                }
-#pragma unroll
-                for (int n8 = 0; n8 < 8; ++n8) {
-                    const int64_t kl = k0 + 8 * n8 + 2 * lk;
-                    if (kl >= a.dl) continue;
-                    const bool has_y = kl + 1 < a.dl;
-                    const double2 o0 = abs[8 * n8 + 2 * lk];
-                    const double2 o1 = abs[8 * n8 + 2 * lk + 1];
-                    double zx = zp[n8].x, zy = zp[n8].y;
-                    double scx = -(zx - c.alpha * acc[n8][0]) * ib2;
-                    double scy = -(zy - c.alpha * acc[n8][1]) * ib2;
-                    if (a.obs_atan) {
-                        scx += c.damp * ((o0.y - o0.x * atan(zx)) / (1.0 + zx * zx));
-                        scy += c.damp * ((o1.y - o1.x * atan(zy)) / (1.0 + zy * zy));
-                    } else {
-                        scx += c.damp * (o0.y - o0.x * zx);
-                        scy += c.damp * (o1.y - o1.x * zy);
-                    }
-                    const uint64_t n0 =
-                        uint64_t(step + 1) * uint64_t(a.d_total) + uint64_t(a.k0 + kl);
-                    double2 xi;
-                    if (kF32Noise) {
-                        const float2 f = normal_pair_f32(n0, uint32_t(i), a.cycle_lo, a.key0, a.key1);
-                        xi = make_double2(f.x, f.y);
-                    } else {
-                        xi = normal_pair_f64(n0, uint32_t(i), a.cycle_lo, a.key0, a.key1);
-                    }
-                    zx += -(c.b * zx - c.s2 * scx) * c.dt + c.sig * xi.x;
-                    zy += -(c.b * zy - c.s2 * scy) * c.dt + c.sig * xi.y;
-                    if (aligned && has_y) {
-                        *reinterpret_cast<double2*>(zrow + kl) = make_double2(zx, zy);
-                    } else {
-                        zrow[kl] = zx;
-                        if (has_y) zrow[kl + 1] = zy;
-                    }
-                    if (!isfinite(zx) || (has_y && !isfinite(zy)))
-                        atomicMin(status, (uint64_t(i) << 32) | uint32_t(step));
-                }
-            }
+            joint_update_epilogue<kF32Noise>(a, c, step, i, k0, lk, acc, abs, z, status);
         }
         __syncthreads();  // every warp is done with this X buffer
+    }
+}
+
+// N > 64: the same tensor-core update with the GEMM's K (members) and the
+// particles tiled.  Work item = (64-coordinate tile, group of 64 particles),
+// consecutive items share the member tile; per item the members stream in
+// chunks of 32: a W block [64 particles][32 members] and an X block
+// [32 members][64 coordinates] per stage, cp.async double-buffered over the
+// flattened (item, chunk) sequence.  W (N x N fp64) stays L2-resident.
+constexpr int kBigK = 32, kBigLdw = 36;
+
+template <bool kF32Noise>
+__global__ void __launch_bounds__(256, 2) joint_apply_tc_big_kernel(
+    KernelArgs a, const double* __restrict__ x, const double2* __restrict__ ab,
+    const double* __restrict__ wn, StepF64 c, int step, double* __restrict__ z,
+    unsigned long long* __restrict__ status, int64_t ntiles) {
+    extern __shared__ double jsm[];
+    const int m = a.m;
+    const int ngroups = (m + 63) / 64, nchunk = (m + kBigK - 1) / kBigK;
+    const size_t wsz = size_t(64) * kBigLdw, xsz = size_t(kBigK) * kTcLdx;
+    double* const W0 = jsm;                                  // [2][64][kBigLdw]
+    double* const X0 = W0 + 2 * wsz;                         // [2][kBigK][kTcLdx]
+    double2* const AB = reinterpret_cast<double2*>(X0 + 2 * xsz);  // [64] of the item's tile
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int lr = lane >> 2, lk = lane & 3;
+    const bool aligned = (a.dl & 1) == 0;
+    const int64_t nitems = ntiles * ngroups;
+    const int64_t my_items = (nitems - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int64_t nseq = my_items * nchunk;
+
+    const auto issue = [&](int64_t sq, int b) {
+        const int64_t item = blockIdx.x + (sq / nchunk) * gridDim.x;
+        const int kc = int(sq % nchunk);
+        const int64_t tile = item / ngroups;
+        const int g = int(item % ngroups);
+        const int64_t k0 = tile * 64;
+        double* Ws = W0 + b * wsz;
+        double* Xs = X0 + b * xsz;
+        for (int q = tid; q < 64 * (kBigK / 2); q += nt) {  // W block, 16 B per copy
+            const int r = q / (kBigK / 2), cc = 2 * (q % (kBigK / 2));
+            const int gi = 64 * g + r, gj = kBigK * kc + cc;
+            double* dst = Ws + r * kBigLdw + cc;
+            if (gi < m && gj + 1 < m) {
+                cp_async16(dst, wn + size_t(gi) * m + gj);
+            } else {
+                dst[0] = (gi < m && gj < m) ? wn[size_t(gi) * m + gj] : 0.0;
+                dst[1] = 0.0;
+            }
+        }
+        for (int q = tid; q < kBigK * 32; q += nt) {  // X block, 16 B per copy
+            const int j = q >> 5, l = q & 31;
+            const int gj = kBigK * kc + j;
+            const int64_t k = k0 + 2 * l;
+            double* dst = Xs + j * kTcLdx + 2 * l;
+            const double* row = x + size_t(gj) * size_t(a.dl);
+            if (gj < m && aligned && k + 1 < a.dl) {
+                cp_async16(dst, row + k);
+            } else {
+                dst[0] = (gj < m && k < a.dl) ? __ldg(row + k) : 0.0;
+                dst[1] = (gj < m && k + 1 < a.dl) ? __ldg(row + k + 1) : 0.0;
+            }
+        }
+        cp_async_commit();
+    };
+
+    double acc[8][2];
+    if (nseq > 0) issue(0, 0);
+    for (int64_t sq = 0; sq < nseq; ++sq) {
+        const int b = int(sq & 1);
+        const int kc = int(sq % nchunk);
+        const int64_t item = blockIdx.x + (sq / nchunk) * gridDim.x;
+        const int64_t tile = item / ngroups;
+        const int g = int(item % ngroups);
+        const int64_t k0 = tile * 64;
+        if (kc == 0) {
+#pragma unroll
+            for (int n8 = 0; n8 < 8; ++n8) acc[n8][0] = acc[n8][1] = 0.0;
+            for (int q = tid; q < 64; q += nt)
+                AB[q] = k0 + q < a.dl ? ab[k0 + q] : make_double2(0.0, 0.0);
+        }
+        if (sq + 1 < nseq) {
+            issue(sq + 1, b ^ 1);  // released by the previous stage's barrier
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* Ws = W0 + b * wsz;
+        const double* Xs = X0 + b * xsz;
+        for (int kq = 0; kq < kBigK; kq += 4) {
+            const double av = Ws[(8 * warp + lr) * kBigLdw + kq + lk];
+            const double* xb = Xs + (kq + lk) * kTcLdx + lr;
+#pragma unroll
+            for (int n8 = 0; n8 < 8; ++n8) dmma_8x8x4(acc[n8], av, xb[8 * n8]);
+        }
+        if (kc == nchunk - 1)
+            joint_update_epilogue<kF32Noise>(a, c, step, 64 * g + 8 * warp + lr, k0, lk, acc, AB, z,
+                                             status);
+        __syncthreads();  // stage buffers (and AB) released
     }
 }
 
@@ -524,6 +635,25 @@ cudaError_t launch_joint_update(const KernelArgs& a, const double* x, const doub
         const int64_t ntiles = (a.dl + 63) / 64;
         const int64_t grid = std::min<int64_t>(ntiles, int64_t(std::max(ps, 1)) * nsm);
         kern<<<unsigned(grid), threads, smem, st>>>(a, x, ab, wn, c, step, z, status, ntiles);
+        return cudaGetLastError();
+    }
+    if (tc_env) {
+        const size_t smem = sizeof(double) * (2 * size_t(64) * kBigLdw + 2 * size_t(kBigK) * kTcLdx) +
+                            sizeof(double2) * 64;
+        auto kern = f32_noise ? joint_apply_tc_big_kernel<true> : joint_apply_tc_big_kernel<false>;
+        if (smem > 48 * 1024) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            if (e != cudaSuccess) return e;
+        }
+        int dev = 0, nsm = 0, ps = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, 256, smem);
+        if (e != cudaSuccess) return e;
+        const int64_t ntiles = (a.dl + 63) / 64;
+        const int64_t items = ntiles * ((a.m + 63) / 64);
+        const int64_t grid = std::min<int64_t>(items, int64_t(std::max(ps, 1)) * nsm);
+        kern<<<unsigned(grid), 256, smem, st>>>(a, x, ab, wn, c, step, z, status, ntiles);
         return cudaGetLastError();
     }
     const dim3 grid(unsigned((a.dl + 63) / 64), unsigned((a.m + kJP * kJW - 1) / (kJP * kJW)));
