@@ -25,6 +25,7 @@ CONFIGS = [
     ("64x64x2 N=20 identity (config 1 grid)", 64, 20, 1),
     ("128x128x2 N=40 stride 4", 128, 40, 4),
     ("256x256x2 N=64 stride 4 (config 2 grid)", 256, 64, 4),
+    ("1024x1024x2 N=64 stride 4 (config 5 grid)", 1024, 64, 4),
 ]
 
 
