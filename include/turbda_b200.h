@@ -77,7 +77,9 @@ typedef enum turbda_precision {
 #define TURBDA_INPUTS_ON_DEVICE 0x1u /* every array pointer is a device pointer  */
 #define TURBDA_ASYNC 0x2u            /* device mode only: do not synchronize;     */
                                      /* fetch the divergence verdict later with   */
-                                     /* turbda_ensf_check()                       */
+                                     /* turbda_ensf_check().  A later call on     */
+                                     /* another stream of the same device waits   */
+                                     /* for it (the scratch is per device)        */
 #define TURBDA_R_UNIFORM 0x4u        /* r_diag points to ONE error variance used  */
                                      /* for every observation (the scalar `r` of  */
                                      /* the Python binding, bindings/python/      */

@@ -95,6 +95,10 @@ struct Workspace {
     std::vector<cudaStream_t> cstreams;         // host-mode chunk pipeline
     std::vector<cudaEvent_t> ev_chunk;
     cudaEvent_t ev_ready = nullptr;
+    // the scratch above is shared by every call on this device: an
+    // asynchronous call leaves its stream here and its completion in ev_done
+    cudaStream_t pending = nullptr;
+    cudaEvent_t ev_done = nullptr;
     // cached step table / batch table keys
     std::vector<unsigned char> steps_key, batch_key;
     // last analysis (for turbda_ensf_check)
@@ -121,8 +125,27 @@ int ws_init(Workspace* w, turbda_status* st) {
         TB_CUDA(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
         TB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->status_host), 64));
         TB_CUDA(cudaEventCreateWithFlags(&w->ev_ready, cudaEventDisableTiming));
+        TB_CUDA(cudaEventCreateWithFlags(&w->ev_done, cudaEventDisableTiming));
     }
     return TURBDA_OK;
+}
+
+// A call on stream s may reuse the workspace only after an earlier
+// asynchronous call (TURBDA_ASYNC) on another stream has finished with it.
+cudaError_t ws_acquire(Workspace* w, cudaStream_t s) {
+    if (w->pending && w->pending != s) return cudaStreamWaitEvent(s, w->ev_done, 0);
+    return cudaSuccess;
+}
+
+// an asynchronous call hands the workspace over with its completion event;
+// a synchronous one has drained it
+cudaError_t ws_release(Workspace* w, cudaStream_t s, bool async) {
+    if (!async) {
+        w->pending = nullptr;
+        return cudaSuccess;
+    }
+    w->pending = s;
+    return cudaEventRecord(w->ev_done, s);
 }
 
 // proj/src/ensf.cpp:149,183-190 and proj/include/turbda/ensf.hpp:15-20
@@ -334,6 +357,7 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
     // stream, where the caller's buffers were most likely produced); host
     // mode runs on the workspace streams
     cudaStream_t s = user_stream ? user_stream : (on_dev ? cudaStreamLegacy : w->stream);
+    TB_CUDA(ws_acquire(w, s));
 
     const int m = p->n_members;
     const int64_t dl = win.dl;
@@ -497,7 +521,10 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
     w->last_steps = p->n_steps;
     w->last_eps = p->eps;
 
-    if (on_dev && (p->flags & TURBDA_ASYNC)) return TURBDA_OK;
+    if (on_dev && (p->flags & TURBDA_ASYNC)) {
+        TB_CUDA(ws_release(w, s, true));
+        return TURBDA_OK;
+    }
 
     if (!on_dev) {
         // results back per chunk, in chunk order (for pageable destinations
@@ -527,6 +554,7 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
     TB_CUDA(cudaMemcpyAsync(w->status_host, dstatus, sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, s));
     TB_CUDA(cudaStreamSynchronize(s));
+    TB_CUDA(ws_release(w, s, false));
     return diverged(p, *w->status_host, st);
 }
 
@@ -604,6 +632,7 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
     std::lock_guard<std::mutex> lk(w->mu);
     if (int rc = ws_init(w, st)) return rc;
     cudaStream_t s = user_stream ? user_stream : (on_dev ? cudaStreamLegacy : w->stream);
+    TB_CUDA(ws_acquire(w, s));
     const int m = p->n_members;
     const int64_t dl = win.dl;
     const size_t md = size_t(m) * size_t(std::max<int64_t>(dl, 1));
@@ -705,7 +734,10 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
     }
     TB_CUDA(launch_relax_f64(z, dx, m, dl, p->relax_factor, dout, s));
     g_launches += 3 + 4 * uint64_t(p->n_steps);
-    if (on_dev && (p->flags & TURBDA_ASYNC)) return TURBDA_OK;
+    if (on_dev && (p->flags & TURBDA_ASYNC)) {
+        TB_CUDA(ws_release(w, s, true));
+        return TURBDA_OK;
+    }
     TB_CUDA(cudaMemcpyAsync(w->status_host, dstatus, sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, s));
     if (!on_dev && dl > 0) {
@@ -720,6 +752,7 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
         }
     }
     TB_CUDA(cudaStreamSynchronize(s));
+    TB_CUDA(ws_release(w, s, false));
     return diverged(p, *w->status_host, st);
 }
 
@@ -898,11 +931,13 @@ int turbda_relax_spread(const double* analysis, const double* forecast, int32_t 
     std::lock_guard<std::mutex> lk(w->mu);
     if (int rc = ws_init(w, st)) return rc;
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : w->stream;
+    TB_CUDA(ws_acquire(w, s));
     const size_t md = size_t(m) * size_t(d);
     if (flags & TURBDA_INPUTS_ON_DEVICE) {
         TB_CUDA(launch_relax_f64(analysis, forecast, m, d, factor, out, s));
         ++g_launches;
         TB_CUDA(cudaStreamSynchronize(s));
+        TB_CUDA(ws_release(w, s, false));
         return TURBDA_OK;
     }
     TB_CUDA(w->x.reserve(sizeof(double) * std::max<size_t>(md, 1)));
@@ -915,6 +950,7 @@ int turbda_relax_spread(const double* analysis, const double* forecast, int32_t 
     ++g_launches;
     TB_CUDA(cudaMemcpyAsync(out, w->out.p, sizeof(double) * md, cudaMemcpyDeviceToHost, s));
     TB_CUDA(cudaStreamSynchronize(s));
+    TB_CUDA(ws_release(w, s, false));
     return TURBDA_OK;
 }
 
@@ -951,6 +987,7 @@ int turbda_score(const double* z, int64_t d, double t, const double* forecast, i
     std::lock_guard<std::mutex> lk(w->mu);
     if (int rc = ws_init(w, st)) return rc;
     cudaStream_t s = w->stream;
+    TB_CUDA(ws_acquire(w, s));
     const size_t md = size_t(m) * size_t(d);
     const size_t d1 = size_t(std::max<int64_t>(d, 1));
     TB_CUDA(w->x.reserve(sizeof(double) * std::max<size_t>(md, 1)));
@@ -991,6 +1028,7 @@ int turbda_score(const double* z, int64_t d, double t, const double* forecast, i
     ++g_launches;
     TB_CUDA(cudaMemcpyAsync(out, w->out.p, sizeof(double) * size_t(d), cudaMemcpyDeviceToHost, s));
     TB_CUDA(cudaStreamSynchronize(s));
+    TB_CUDA(ws_release(w, s, false));
     return TURBDA_OK;
 }
 
@@ -1005,6 +1043,7 @@ int turbda_diag(const double* members, int32_t m, int64_t d, const double* truth
     std::lock_guard<std::mutex> lk(w->mu);
     if (int rc = ws_init(w, st)) return rc;
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : w->stream;
+    TB_CUDA(ws_acquire(w, s));
     TB_CUDA(w->status.reserve(64));
     double* dsum = reinterpret_cast<double*>(w->status.as<unsigned char>() + 16);
     const size_t md = size_t(m) * size_t(d);
@@ -1024,6 +1063,7 @@ int turbda_diag(const double* members, int32_t m, int64_t d, const double* truth
     ++g_launches;
     TB_CUDA(cudaMemcpyAsync(out, dsum, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     TB_CUDA(cudaStreamSynchronize(s));
+    TB_CUDA(ws_release(w, s, false));
     return TURBDA_OK;
 }
 

@@ -339,3 +339,29 @@ def test_joint_mode_multi_process_nccl(capi):
            str(ROOT / "tools" / "joint_multiproc_check.py")]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert "JOINT_MULTIPROC_OK" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
+
+
+def test_async_calls_on_two_streams_do_not_share_scratch(capi):
+    """TURBDA_ASYNC device-mode calls on different streams reuse the device's
+    workspace; the second waits for the first (ws_acquire), so both results
+    equal their synchronous counterparts."""
+    torch = pytest.importorskip("torch")
+    dev = torch.device("cuda:0")
+    outs, wants, streams = [], [], [torch.cuda.Stream(), torch.cuda.Stream()]
+    inputs = [throughput_inputs(32, 8192, stride=4) for _ in range(2)]
+    for (x, y, idx), strm, cyc in zip(inputs, streams, (1, 2)):
+        wants.append(capi.analyze_host(x, y, 1.0, idx, n_steps=60, cycle=cyc))
+        tx = torch.from_numpy(x).to(dev)
+        ty = torch.from_numpy(y).to(dev)
+        tr = torch.ones_like(ty)
+        ti = torch.from_numpy(idx).to(dev)
+        out = torch.empty_like(tx)
+        torch.cuda.synchronize()
+        p = capi.params(d_total=8192, d_local=8192, obs_dim=y.size, n_members=32, n_steps=60,
+                        obs_kind=1, cycle=cyc, device=0,
+                        flags=capi.INPUTS_ON_DEVICE | capi.ASYNC)
+        capi.analyze(p, tx, ty, tr, ti, out, stream=strm.cuda_stream)
+        outs.append((out, tx, ty, tr, ti))
+    torch.cuda.synchronize()
+    for (out, *_), want in zip(outs, wants):
+        assert np.array_equal(out.cpu().numpy(), want)
