@@ -163,6 +163,91 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const double* __restr
         }
 }
 
+// The same partial Gram for N >= 128 with 128 x 128 output tiles (16 warps,
+// each a 16 x 64 block of 2 x 8 DMMA tiles): every Z and X row block is read
+// N/128 instead of N/64 times per pseudo-step, and each k-step feeds 16 DMMA
+// from 10 fragment loads.
+constexpr int kT2 = 128;
+
+__global__ void __launch_bounds__(512) gram_partial_big_kernel(const double* __restrict__ z,
+                                                               const double* __restrict__ x,
+                                                               int n, int m, int64_t dl,
+                                                               int64_t chunk,
+                                                               double* __restrict__ part) {
+    __shared__ double zs[kT2][kStride];
+    __shared__ double xs[kT2][kStride];
+    const int ntj = (m + kT2 - 1) / kT2;
+    const int ti0 = (blockIdx.y / ntj) * kT2, tj0 = (blockIdx.y % ntj) * kT2;
+    const int64_t c0 = int64_t(blockIdx.x) * chunk;
+    const int64_t c1 = c0 + chunk < dl ? c0 + chunk : dl;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wr = 16 * (warp >> 1), wc = 64 * (warp & 1);  // the warp's 16 x 64 block
+    double acc[2][8][2] = {};
+    double nzp[4] = {}, nxp[4] = {};  // rows sr + 32u of this thread's staging column
+    const int sr = threadIdx.x / kK, sc = threadIdx.x % kK;  // sr in [0, 32)
+    double zn[4], xn[4];
+    const auto fetch = [&](int64_t kb) {
+        const int64_t k = kb + sc;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int r = sr + 32 * u;
+            zn[u] = (k < c1 && ti0 + r < n) ? __ldg(z + size_t(ti0 + r) * size_t(dl) + size_t(k)) : 0.0;
+            xn[u] = (k < c1 && tj0 + r < m) ? __ldg(x + size_t(tj0 + r) * size_t(dl) + size_t(k)) : 0.0;
+        }
+    };
+    if (c0 < c1) fetch(c0);
+    for (int64_t kb = c0; kb < c1; kb += kK) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int r = sr + 32 * u;
+            zs[r][sc] = zn[u];
+            xs[r][sc] = xn[u];
+            nzp[u] = fma(zn[u], zn[u], nzp[u]);
+            nxp[u] = fma(xn[u], xn[u], nxp[u]);
+        }
+        __syncthreads();
+        if (kb + kK < c1) fetch(kb + kK);
+#pragma unroll
+        for (int kq = 0; kq < kK / 4; ++kq) {
+            const int kk = 4 * kq + (lane & 3);
+            const double a0 = zs[wr + (lane >> 2)][kk];
+            const double a1 = zs[wr + 8 + (lane >> 2)][kk];
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+                const double b = xs[wc + 8 * nt + (lane >> 2)][kk];
+                dmma_8x8x4(acc[0][nt], a0, b);
+                dmma_8x8x4(acc[1][nt], a1, b);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        for (int o = 8; o > 0; o >>= 1) {
+            nzp[u] += __shfl_xor_sync(0xffffffffu, nzp[u], o);
+            nxp[u] += __shfl_xor_sync(0xffffffffu, nxp[u], o);
+        }
+    double* out = part + size_t(blockIdx.x) * (size_t(n) * m + n + m);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int i = ti0 + wr + 8 * h + (lane >> 2);
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int j = tj0 + wc + 8 * nt + 2 * (lane & 3) + e;
+                if (i < n && j < m) out[size_t(i) * m + j] = acc[h][nt][e];
+            }
+    }
+    if (sc == 0)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int r = sr + 32 * u;
+            if (tj0 == 0 && ti0 + r < n) out[size_t(n) * m + ti0 + r] = nzp[u];
+            if (ti0 == 0 && tj0 + r < m) out[size_t(n) * m + n + tj0 + r] = nxp[u];
+        }
+}
+
 // Fixed-order (deterministic) sum over chunks: stage 1 sums chunk group
 // blockIdx.y (chunks y, y + G, y + 2G, ...) into part2[y]; stage 2 sums the
 // G groups in order.
@@ -563,9 +648,13 @@ __global__ void __launch_bounds__(256, 2) joint_apply_tc_big_kernel(
 
 }  // namespace
 
+// N >= 128: the 128 x 128 tiles of gram_partial_big_kernel
+bool joint_gram_big(int n, int m) { return n >= kT2 && m >= kT2; }
+
 JointPlan joint_plan(int n, int m, int64_t dl) {
     JointPlan pl;
-    const int tiles = ((n + kT - 1) / kT) * ((m + kT - 1) / kT);
+    const int tt = joint_gram_big(n, m) ? kT2 : kT;
+    const int tiles = ((n + tt - 1) / tt) * ((m + tt - 1) / tt);
     pl.nchunk = (296 + tiles - 1) / tiles;  // ~2 CTAs per SM in total
     const int64_t want = (dl + pl.nchunk - 1) / pl.nchunk;
     pl.chunk = (want + kK - 1) / kK * kK;
@@ -588,8 +677,12 @@ cudaError_t launch_joint_init(const KernelArgs& a, double* z, cudaStream_t st) {
 cudaError_t launch_joint_gram(const KernelArgs& a, const JointPlan& pl, const double* z,
                               const double* x, double* part, double* red, cudaStream_t st) {
     if (a.dl > 0) {
-        gram_partial_kernel<<<dim3(unsigned(pl.nchunk), unsigned(pl.tiles)), 256, 0, st>>>(
-            z, x, a.m, a.m, a.dl, pl.chunk, part);
+        if (joint_gram_big(a.m, a.m))
+            gram_partial_big_kernel<<<dim3(unsigned(pl.nchunk), unsigned(pl.tiles)), 512, 0, st>>>(
+                z, x, a.m, a.m, a.dl, pl.chunk, part);
+        else
+            gram_partial_kernel<<<dim3(unsigned(pl.nchunk), unsigned(pl.tiles)), 256, 0, st>>>(
+                z, x, a.m, a.m, a.dl, pl.chunk, part);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         double* part2 = part + size_t(pl.nchunk) * pl.red_len;

@@ -280,7 +280,8 @@ def test_arctan_python_binding(capi, port):
 JOINT_TOL = 1e-9
 
 
-@pytest.mark.parametrize("m,d,stride", [(20, 1024, 1), (64, 3000, 4), (33, 257, 1), (80, 700, 3)])
+@pytest.mark.parametrize("m,d,stride", [(20, 1024, 1), (64, 3000, 4), (33, 257, 1), (80, 700, 3),
+                                          (160, 600, 2)])
 def test_joint_mode_vs_port(capi, port, m, d, stride):
     x, y, idx, _ = conditioned_inputs(m, d, stride=stride)
     # weak obs and a wide prior keep the joint softmax away from one-hot
