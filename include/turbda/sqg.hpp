@@ -3,9 +3,9 @@
 // forecast surface of the reference class (grid, params, CFL tracking) over
 // a batch of states advanced together on the device (batched fp64 cuFFT,
 // integrating-factor RK4 captured as a CUDA graph, csrc/sqg_gpu.cu via the
-// C-ABI turbda_sqg_*).  The reference's spectral diagnostics
-// (forward_transform, tendency, ke_spectrum, ...) serve the CLI / ViT budget
-// and are not part of this build.
+// C-ABI turbda_sqg_*), plus the kinetic-energy spectrum and its log-log
+// slope fit (proj/src/sqg.cpp:306-357).  The reference's remaining spectral
+// internals (forward_transform, tendency, ...) are not part of this build.
 #pragma once
 
 #include <cstdint>
@@ -37,6 +37,15 @@ struct SqgParams {
     bool operator==(const SqgParams&) const = default;
 };
 
+struct KeBin {
+    double kappa;
+    double energy;
+};
+
+// least-squares log-log slope over shells [lo_shell, hi_shell] (zero bins
+// skipped); ConfigError when fewer than two usable bins remain
+double fit_loglog_slope(const std::vector<KeBin>& spectrum, int lo_shell, int hi_shell);
+
 class SqgModel {
 public:
     // `batch` states of [2][ny][nx] advanced together on `device` (-1: current)
@@ -49,6 +58,10 @@ public:
     // non-negative multiple of dt; 0 is the exact identity).  ConfigError
     // for other durations; BlowupError(t, member) on a non-finite state.
     void advance(double* states, double hours);
+
+    // shell-summed kinetic energy of ONE host state [2 ny nx] (bins at
+    // kappa = s 2 pi / lx); ConfigError unless lx == ly
+    std::vector<KeBin> ke_spectrum(const double* state);
 
     double max_cfl() const { return max_cfl_; }
     void reset_cfl() { max_cfl_ = 0.0; }

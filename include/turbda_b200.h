@@ -232,6 +232,17 @@ TURBDA_API int turbda_sqg_create(const turbda_sqg_params* p, int32_t batch, int3
 TURBDA_API int turbda_sqg_advance(void* handle, double* states, double hours, uint32_t flags, void* stream,
                        double* max_cfl, turbda_status* status);
 TURBDA_API int turbda_sqg_destroy(void* handle);
+/* shell-summed kinetic energy of ONE state [2][ny][nx] (host, or device with
+ * TURBDA_INPUTS_ON_DEVICE): bins kappa = s 2 pi / lx (SqgModel::ke_spectrum,
+ * proj/src/sqg.cpp:306-335); *n_bins = shells, up to max_bins written */
+TURBDA_API int turbda_sqg_ke_spectrum(void* handle, const double* state, uint32_t flags,
+                                      double* kappa, double* energy, int32_t max_bins,
+                                      int32_t* n_bins, turbda_status* status);
+/* log-log least-squares slope over shells [lo, hi], empty bins skipped
+ * (fit_loglog_slope, proj/src/sqg.cpp:337-357); TURBDA_CONFIG with < 2 bins */
+TURBDA_API int turbda_fit_loglog_slope(const double* kappa, const double* energy, int32_t n,
+                                       int32_t lo_shell, int32_t hi_shell, double* slope,
+                                       turbda_status* status);
 /* nature_run: snapshots [n][2][ny][nx] into host memory */
 TURBDA_API int turbda_nature_run(const turbda_sqg_params* p, double spinup, double duration,
                       double interval, uint64_t seed, double* snapshots, int32_t max_snaps,

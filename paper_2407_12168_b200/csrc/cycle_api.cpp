@@ -84,6 +84,32 @@ void SqgModel::advance(double* states, double hours) {
     if (rc) raise_sqg(rc, st);
 }
 
+std::vector<KeBin> SqgModel::ke_spectrum(const double* state) {
+    const int cap = grid_.nx + grid_.ny + 8;  // > number of shells
+    std::vector<double> k(static_cast<size_t>(cap)), e(static_cast<size_t>(cap));
+    int32_t n = 0;
+    turbda_status st{};
+    if (int rc = turbda_sqg_ke_spectrum(handle_, state, 0u, k.data(), e.data(), cap, &n, &st))
+        raise_sqg(rc, st);
+    std::vector<KeBin> bins(static_cast<size_t>(n));
+    for (int s = 0; s < n; ++s) bins[size_t(s)] = {k[size_t(s)], e[size_t(s)]};
+    return bins;
+}
+
+double fit_loglog_slope(const std::vector<KeBin>& spectrum, int lo_shell, int hi_shell) {
+    std::vector<double> k, e;
+    for (const KeBin& b : spectrum) {
+        k.push_back(b.kappa);
+        e.push_back(b.energy);
+    }
+    double slope = 0.0;
+    turbda_status st{};
+    if (int rc = turbda_fit_loglog_slope(k.data(), e.data(), int32_t(k.size()), lo_shell, hi_shell,
+                                         &slope, &st))
+        raise_sqg(rc, st);
+    return slope;
+}
+
 // ------------------------------------------------------------- forecast -----
 SqgStepper::SqgStepper(const GridSpec& grid, const SqgParams& params) : model_(grid, params) {}
 

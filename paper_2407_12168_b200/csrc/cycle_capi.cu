@@ -316,6 +316,57 @@ int turbda_sqg_advance(void* handle, double* states, double hours, uint32_t flag
     return TURBDA_OK;
 }
 
+int turbda_sqg_ke_spectrum(void* handle, const double* state, uint32_t flags, double* kappa,
+                           double* energy, int32_t max_bins, int32_t* n_bins, turbda_status* st) {
+    clear(st);
+    auto* m = static_cast<SqgGpu*>(handle);
+    if (!m) return fail(st, TURBDA_CONFIG, "sqg: null handle");
+    cudaStream_t s;
+    CY_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct Guard {
+        cudaStream_t s;
+        ~Guard() { cudaStreamDestroy(s); }
+    } guard{s};
+    const double* dptr = state;
+    DeviceBuffer tmp;
+    if (!(flags & TURBDA_INPUTS_ON_DEVICE)) {
+        const size_t bytes = sizeof(double) * m->state_size();
+        CY_CUDA(cudaMalloc(&tmp.p, bytes));
+        CY_CUDA(cudaMemcpyAsync(tmp.p, state, bytes, cudaMemcpyHostToDevice, s));
+        dptr = tmp.as<double>();
+    }
+    std::vector<double> k, e;
+    const std::string err = m->ke_spectrum(dptr, s, &k, &e);
+    if (!err.empty()) return sqg_error(err, st);
+    const int n = int(k.size());
+    if (n_bins) *n_bins = n;
+    for (int q = 0; q < std::min(n, int(max_bins)); ++q) {
+        if (kappa) kappa[q] = k[size_t(q)];
+        if (energy) energy[q] = e[size_t(q)];
+    }
+    return TURBDA_OK;
+}
+
+// least-squares log-log slope over shells [lo, hi] (proj/src/sqg.cpp:337-357)
+int turbda_fit_loglog_slope(const double* kappa, const double* energy, int32_t n, int32_t lo,
+                            int32_t hi, double* slope, turbda_status* st) {
+    clear(st);
+    double sx = 0.0, sy = 0.0, sxx = 0.0, sxy = 0.0;
+    int used = 0;
+    for (int b = std::max(lo, 0); b <= hi && b < n; ++b) {
+        if (!(energy[b] > 0.0) || !(kappa[b] > 0.0)) continue;  // empty bins skipped
+        const double lx = std::log(kappa[b]), ly = std::log(energy[b]);
+        sx += lx;
+        sy += ly;
+        sxx += lx * lx;
+        sxy += lx * ly;
+        ++used;
+    }
+    if (used < 2) return fail(st, TURBDA_CONFIG, "slope fit needs at least two non-empty bins");
+    if (slope) *slope = (used * sxy - sx * sy) / (used * sxx - sx * sx);
+    return TURBDA_OK;
+}
+
 int turbda_sqg_destroy(void* handle) {
     delete static_cast<SqgGpu*>(handle);
     return TURBDA_OK;

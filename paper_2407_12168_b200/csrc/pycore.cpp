@@ -5,9 +5,9 @@
 // devices; arrays go straight from numpy to the device through the C-ABI.
 // GridSpec / SqgParams, nature_run / advance (:87-109, the GPU model),
 // default_config_json / config_hash (:196-202) and the exceptions (:223-224)
-// follow the reference.  run_experiment lives in experiment.py (the
-// GPU-resident cycle driver).  Out of scope: ke_spectrum / fit_loglog_slope
-// and the ViT budget helpers.
+// follow the reference, as do ke_spectrum / fit_loglog_slope (:111-138).
+// run_experiment lives in experiment.py (the GPU-resident cycle driver).
+// Out of scope: the ViT budget helpers.
 #include <pybind11/numpy.h>
 #include <pybind11/pybind11.h>
 
@@ -227,6 +227,36 @@ PYBIND11_MODULE(_core, mod) {
             return field_array(grid, v);
         },
         py::arg("grid"), py::arg("params"), py::arg("state"), py::arg("hours"));
+
+    mod.def(
+        "ke_spectrum",
+        [](const turbda::GridSpec& grid, const turbda::SqgParams& params, const darray& state) {
+            if (size_t(state.size()) != grid.grid_size())
+                throw turbda::DimensionError("ke_spectrum: state size does not match grid");
+            std::vector<turbda::KeBin> bins;
+            {
+                py::gil_scoped_release nogil;
+                turbda::SqgModel model(grid, params);
+                bins = model.ke_spectrum(state.data());
+            }
+            py::array_t<double> kappa(py::ssize_t(bins.size())), energy(py::ssize_t(bins.size()));
+            for (size_t s = 0; s < bins.size(); ++s) {
+                kappa.mutable_data()[s] = bins[s].kappa;
+                energy.mutable_data()[s] = bins[s].energy;
+            }
+            return py::make_tuple(kappa, energy);
+        },
+        py::arg("grid"), py::arg("params"), py::arg("state"));
+
+    mod.def(
+        "fit_loglog_slope",
+        [](const darray& kappa, const darray& energy, int lo_shell, int hi_shell) {
+            std::vector<turbda::KeBin> bins(size_t(kappa.size()));
+            for (size_t s = 0; s < bins.size(); ++s)
+                bins[s] = {kappa.data()[s], energy.data()[s]};
+            return turbda::fit_loglog_slope(bins, lo_shell, hi_shell);
+        },
+        py::arg("kappa"), py::arg("energy"), py::arg("lo_shell"), py::arg("hi_shell"));
 
     mod.def("letkf_analyze", &letkf_analyze, py::arg("members"), py::arg("grid"), py::arg("y"),
             py::arg("r") = 1.0, py::arg("cutoff_km") = 2000.0, py::arg("rtps_alpha") = 0.3,

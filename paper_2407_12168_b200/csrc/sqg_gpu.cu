@@ -155,6 +155,28 @@ __global__ void sqg_scale_mask(cufftDoubleComplex* __restrict__ th, const double
     th[q].y *= w;
 }
 
+// per-mode kinetic energy of one state for ke_spectrum (proj/src/sqg.cpp:306-335):
+// theta_hat (scaled forward transform, no dealias) -> psi -> 0.5 w |k p|^2 / nz,
+// out [lev][mode]; the shell sums run on the host in the reference's order
+__global__ void sqg_mode_energy(const cufftDoubleComplex* __restrict__ th, ModeTables t,
+                                int nmode, int nkx, int nx, double scale,
+                                double* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nmode) return;
+    const double t0r = th[i].x * scale, t0i = th[i].y * scale;
+    const double t1r = th[nmode + i].x * scale, t1i = th[nmode + i].y * scale;
+    const double pr[2] = {t.i00[i] * t0r + t.i01[i] * t1r, -t.i01[i] * t0r + t.i11[i] * t1r};
+    const double pi[2] = {t.i00[i] * t0i + t.i01[i] * t1i, -t.i01[i] * t0i + t.i11[i] * t1i};
+    const int jx = i % nkx;
+    const double w = (jx == 0 || jx == nx / 2) ? 1.0 : 2.0;
+    const double kx = t.kx[i], ky = t.ky[i];
+    for (int lev = 0; lev < 2; ++lev) {
+        const double ar = ky * pr[lev], ai = ky * pi[lev], br = kx * pr[lev], bi = kx * pi[lev];
+        const double u2 = (ar * ar + ai * ai) + (br * br + bi * bi);
+        out[size_t(lev) * nmode + i] = 0.5 * w * u2 / 2.0;
+    }
+}
+
 }  // namespace
 
 struct SqgGpu::Impl {
@@ -172,6 +194,8 @@ struct SqgGpu::Impl {
     cudaStream_t own = nullptr;  // capture / replay stream (the legacy stream cannot be captured)
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     cudaGraphExec_t step_graph = nullptr;
+    std::vector<double> hkx, hky;     // host copies of the wavenumber tables
+    cufftHandle r2c_one = 0;          // one state (2 planes), ke_spectrum
 };
 
 static void free_all(SqgGpu::Impl* p) {
@@ -183,6 +207,7 @@ static void free_all(SqgGpu::Impl* p) {
     if (p->r2c_ten) cufftDestroy(p->r2c_ten);
     if (p->r2c_state) cufftDestroy(p->r2c_state);
     if (p->c2r_state) cufftDestroy(p->c2r_state);
+    if (p->r2c_one) cufftDestroy(p->r2c_one);
     cudaFree(p->tables);
     cudaFree(p->th);
     cudaFree(p->ks);
@@ -252,6 +277,8 @@ std::string SqgGpu::init(const SqgConfig& c, int batch) {
     }
     if (cudaMalloc(&p.tables, sizeof(double) * h.size()) != cudaSuccess) return "cudaMalloc tables";
     cudaMemcpy(p.tables, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice);
+    p.hkx.assign(kx, kx + nmode);
+    p.hky.assign(ky, ky + nmode);
     p.t = ModeTables{p.tables, p.tables + nmode, p.tables + 2 * nmode, p.tables + 3 * nmode,
                      p.tables + 4 * nmode, p.tables + 5 * nmode, p.tables + 6 * nmode,
                      p.tables + 7 * nmode};
@@ -287,6 +314,45 @@ std::string SqgGpu::init(const SqgConfig& c, int batch) {
 }
 
 int SqgGpu::batch() const { return impl_ ? impl_->nb : 0; }
+
+// proj/src/sqg.cpp:306-335: shell-summed kinetic energy of ONE state
+// [2][ny][nx] on the device; bins at kappa = s 2 pi / lx, s = round(|k| / dk)
+std::string SqgGpu::ke_spectrum(const double* state, cudaStream_t st, std::vector<double>* kappa,
+                                std::vector<double>* energy) {
+    Impl& p = *impl_;
+    const SqgConfig& c = p.cfg;
+    if (c.lx != c.ly) return "config:ke_spectrum: requires lx == ly";
+    if (!p.r2c_one) {
+        int n2[2] = {c.ny, c.nx};
+        if (cufftPlanMany(&p.r2c_one, 2, n2, nullptr, 1, p.npix, nullptr, 1, p.nmode, CUFFT_D2Z, 2) !=
+            CUFFT_SUCCESS)
+            return "cufftPlanMany";
+    }
+    cufftSetStream(p.r2c_one, st);
+    if (cufftExecD2Z(p.r2c_one, const_cast<double*>(state), p.cwork) != CUFFT_SUCCESS)
+        return "cufftExecD2Z";
+    const int nkx = c.nx / 2 + 1;
+    sqg_mode_energy<<<unsigned((p.nmode + 255) / 256), 256, 0, st>>>(
+        p.cwork, p.t, p.nmode, nkx, c.nx, 1.0 / (double(c.nx) * c.ny), p.gten);
+    if (cudaGetLastError() != cudaSuccess) return "sqg_mode_energy";
+    std::vector<double> e(size_t(2) * p.nmode);
+    if (cudaMemcpyAsync(e.data(), p.gten, sizeof(double) * e.size(), cudaMemcpyDeviceToHost, st) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return "ke_spectrum copy";
+    const double dk = kTwoPi / c.lx;
+    const double kmax = std::hypot(kTwoPi * (c.nx / 2) / c.lx, kTwoPi * (c.ny / 2) / c.ly);
+    const int nshell = int(std::lround(kmax / dk)) + 1;
+    kappa->assign(size_t(nshell), 0.0);
+    energy->assign(size_t(nshell), 0.0);
+    for (int s = 0; s < nshell; ++s) (*kappa)[size_t(s)] = s * dk;
+    for (int lev = 0; lev < 2; ++lev)  // the reference's summation order
+        for (int i = 0; i < p.nmode; ++i) {
+            const int s = int(std::lround(std::hypot(p.hkx[size_t(i)], p.hky[size_t(i)]) / dk));
+            (*energy)[size_t(s)] += e[size_t(lev) * p.nmode + i];
+        }
+    return "";
+}
 
 size_t SqgGpu::state_size() const { return impl_ ? size_t(2) * impl_->npix : 0; }
 

@@ -5,6 +5,7 @@
 
 #include <memory>
 #include <string>
+#include <vector>
 
 namespace tb200 {
 
@@ -33,6 +34,9 @@ public:
     // non-finite state *blown_member / *blown_hours report the first one.
     std::string advance(double* states, double hours, cudaStream_t st, double* max_cfl,
                         int* blown_member, double* blown_hours);
+    // shell-summed kinetic energy of one device state [2][ny][nx]
+    std::string ke_spectrum(const double* state, cudaStream_t st, std::vector<double>* kappa,
+                            std::vector<double>* energy);
 
 private:
     std::unique_ptr<Impl> impl_;

@@ -41,7 +41,7 @@ def test_binding_surface():
     import paper_2407_12168_b200 as tb
     for name in ("GridSpec", "SqgParams", "nature_run", "advance", "ensf_analyze",
                  "letkf_analyze", "run_experiment", "default_config_json", "config_hash",
-                 "ConfigError", "DimensionError"):
+                 "ke_spectrum", "fit_loglog_slope", "ConfigError", "DimensionError"):
         assert hasattr(tb, name), name
     p = tb.SqgParams()
     assert (p.f, p.n, p.u0, p.hyper_order, p.dt) == (1.0, 10.0, 0.1, 4, 0.25)
@@ -56,6 +56,21 @@ def _grid(tb, n=16):
     return g
 
 
+def test_fit_loglog_slope_matches_reference(ref):
+    import paper_2407_12168_b200 as tb
+    rng = np.random.default_rng(3)
+    kappa = np.arange(12) * 0.3
+    energy = np.abs(rng.standard_normal(12)) * np.concatenate([[0.0], kappa[1:] ** -3.0])
+    energy[5] = 0.0  # empty bins (and kappa = 0) are skipped
+    got = ref.run("out['s'] = ref.fit_loglog_slope(kappa, energy, 1, 10)\n"
+                  "out['t'] = ref.fit_loglog_slope(kappa, energy, -3, 40)",
+                  kappa=kappa, energy=energy)
+    assert tb.fit_loglog_slope(kappa, energy, 1, 10) == pytest.approx(got["s"], rel=1e-14)
+    assert tb.fit_loglog_slope(kappa, energy, -3, 40) == pytest.approx(got["t"], rel=1e-14)
+    with pytest.raises(tb.ConfigError):
+        tb.fit_loglog_slope(kappa, energy, 5, 6)
+
+
 @pytest.mark.gpu
 def test_model_calls_match_reference(ref):
     import paper_2407_12168_b200 as tb
@@ -64,13 +79,16 @@ def test_model_calls_match_reference(ref):
         "p = ref.SqgParams()\n"
         "snaps = ref.nature_run(g, p, 48.0, 24.0, 12.0, 3)\n"
         "out['snaps'] = np.stack(snaps)\n"
-        "out['adv'] = ref.advance(g, p, snaps[-1], 6.0)", L=L16)
+        "out['adv'] = ref.advance(g, p, snaps[-1], 6.0)\n"
+        "out['k'], out['e'] = ref.ke_spectrum(g, p, snaps[-1])", L=L16)
     g, p = _grid(tb), tb.SqgParams()
     snaps = np.stack(tb.nature_run(g, p, 48.0, 24.0, 12.0, 3))
     assert snaps.shape == got["snaps"].shape == (3, 2, 16, 16)
     assert rel_l2(snaps, got["snaps"]) < 1e-9
     adv = tb.advance(g, p, got["snaps"][-1], 6.0)
     assert adv.shape == (2, 16, 16) and rel_l2(adv, got["adv"]) < 1e-11
+    k, e = tb.ke_spectrum(g, p, got["snaps"][-1])
+    assert np.array_equal(k, got["k"]) and rel_l2(e, got["e"]) < 1e-12
 
 
 @pytest.mark.gpu
