@@ -6,15 +6,17 @@
 // GridSpec / SqgParams, nature_run / advance (:87-109, the GPU model),
 // default_config_json / config_hash (:196-202) and the exceptions (:223-224)
 // follow the reference, as do ke_spectrum / fit_loglog_slope (:111-138).
-// run_experiment lives in experiment.py (the GPU-resident cycle driver).
-// Out of scope: the ViT budget helpers.
+// run_experiment lives in experiment.py (the GPU-resident cycle driver);
+// the budget helpers (:204-220) are plain host arithmetic.
 #include <pybind11/numpy.h>
 #include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
 
 #include <cmath>
 #include <string>
 #include <vector>
 
+#include "turbda/budget.hpp"
 #include "turbda/config.hpp"
 #include "turbda/errors.hpp"
 #include "turbda/forecast.hpp"
@@ -269,6 +271,24 @@ PYBIND11_MODULE(_core, mod) {
     mod.def("config_hash", [](const std::string& config_json) {
         return turbda::config_hash(turbda::config_from_json(nlohmann::json::parse(config_json)));
     });
+
+    mod.def("vit_param_count", &turbda::vit_param_count, py::arg("layers"), py::arg("embed_dim"),
+            py::arg("mlp_ratio"));
+    mod.def(
+        "estimate_training_flops",
+        [](const std::vector<long long>& input_dims, const std::vector<long long>& patch_dims,
+           double epochs, double params, double images) {
+            turbda::BudgetSpec spec;
+            spec.input_dims = input_dims;
+            spec.patch_dims = patch_dims;
+            spec.epochs = epochs;
+            spec.params = params;
+            spec.dataset_images = images;
+            return turbda::estimate_training_flops(spec);
+        },
+        py::arg("input_dims"), py::arg("patch_dims"), py::arg("epochs"), py::arg("params"),
+        py::arg("images"));
+    mod.def("format_sig", &turbda::format_sig, py::arg("x"), py::arg("digits") = 4);
 
     mod.def("device_count", &turbda_device_count);
     mod.def("build_arch", [] { return std::string(turbda_build_arch()); });

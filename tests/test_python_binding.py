@@ -41,7 +41,8 @@ def test_binding_surface():
     import paper_2407_12168_b200 as tb
     for name in ("GridSpec", "SqgParams", "nature_run", "advance", "ensf_analyze",
                  "letkf_analyze", "run_experiment", "default_config_json", "config_hash",
-                 "ke_spectrum", "fit_loglog_slope", "ConfigError", "DimensionError"):
+                 "ke_spectrum", "fit_loglog_slope", "vit_param_count", "estimate_training_flops",
+                 "format_sig", "ConfigError", "DimensionError"):
         assert hasattr(tb, name), name
     p = tb.SqgParams()
     assert (p.f, p.n, p.u0, p.hyper_order, p.dt) == (1.0, 10.0, 0.1, 4, 0.25)
@@ -54,6 +55,20 @@ def _grid(tb, n=16):
     g.nx = g.ny = n
     g.lx = g.ly = L16 * n / 16
     return g
+
+
+def test_budget_helpers_match_reference(ref):
+    import paper_2407_12168_b200 as tb
+    got = ref.run("out['p'] = ref.vit_param_count(24, 2048, 4.0)\n"
+                  "out['f'] = ref.estimate_training_flops([256, 256], [4, 4], 100.0, 2.5e9, 1e6)\n"
+                  "out['s'] = [ref.format_sig(v, d) for v, d in ((1.208e9, 4), (6.144e21, 3),"
+                  " (0.0, 4), (-3.25e-7, 2), (999.96, 4))]")
+    assert tb.vit_param_count(24, 2048, 4.0) == got["p"]
+    assert tb.estimate_training_flops([256, 256], [4, 4], 100.0, 2.5e9, 1e6) == got["f"]
+    assert [tb.format_sig(v, d) for v, d in ((1.208e9, 4), (6.144e21, 3), (0.0, 4),
+                                            (-3.25e-7, 2), (999.96, 4))] == got["s"]
+    with pytest.raises(tb.ConfigError):
+        tb.estimate_training_flops([256, 255], [4, 4], 1.0, 1.0, 1.0)
 
 
 def test_fit_loglog_slope_matches_reference(ref):

@@ -1,6 +1,6 @@
 """The reference's own unit tests for the path and the widened rows
-(proj/tests/test_{ensf,rng,ensemble,parallel,snapshot,forecast,osse}.cpp,
-65 cases), compiled unmodified against
+(proj/tests/test_{ensf,rng,ensemble,parallel,snapshot,forecast,osse,budget}.cpp,
+72 cases), compiled unmodified against
 include/turbda/*.hpp and linked to libturbda_b200.so (oracle/reftests) -
 the drop-in check for the C++ API.
 
@@ -49,6 +49,8 @@ def test_host_only_reference_cases():
                  "operator locations", "observation validation", "ensemble validation",
                  "snapshot round", "snapshot header", "corrupt", "snapshot file", "config json",
                  "partial configs", "config hash", "experiment config", "model error config",
+                 "parameter count", "published", "tokens per image", "training", "budget",
+                 "significant",
                  "metrics serialization"):
         passed, failed, out = _run(filt)
         assert passed | failed, filt
@@ -59,13 +61,13 @@ def test_host_only_reference_cases():
 def test_reference_suite_on_b200():
     passed, failed, out = _run()
     print(out[-3000:])
-    assert len(passed) + len(failed) == 65
+    assert len(passed) + len(failed) == 72
     assert failed == EXPECTED_FAILURES, out
 
 
 @pytest.mark.gpu
 def test_reference_suite_same_verdicts_as_reference():
-    """The same 65 cases linked against the reference implementation (the
+    """The same 72 cases linked against the reference implementation (the
     cycle oracle, cuFFTW build) fail exactly where the B200 build fails."""
     passed_r, failed_r, out_r = _run(binary=REF_BIN)
     passed, failed, _ = _run()
