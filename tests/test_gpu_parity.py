@@ -241,6 +241,46 @@ def test_cfg2_full_size_properties(capi):
     assert np.array_equal(np.concatenate([lo, hi], axis=1), a32)
 
 
+@pytest.mark.slow
+def test_cfg3_full_size_window_vs_port(capi, port):
+    """BASELINE config 3 at full size (d = 16.8M, N = 20, S = 100, identity
+    obs) on one GPU; a 2,048-coordinate window deep inside the state is
+    recomputed by the C restatement (bit-exact with the reference, noise
+    keyed by the global coordinate) and must agree to the fp32 tolerance."""
+    d, m = 16_777_216, 20
+    g = np.random.default_rng(11)
+    x = g.standard_normal((m, d), dtype=np.float32).astype(np.float64)
+    y = g.standard_normal(d, dtype=np.float32).astype(np.float64)
+    got = capi.analyze_host(x, y, 1.0, None)
+    assert np.isfinite(got).all()
+    k0, w = 10_000_000, 2048
+    want = port.analyze(x[:, k0:k0 + w], y[k0:k0 + w], 1.0, None, k0=k0, d_total=d)
+    assert rel_l2(got[:, k0:k0 + w], want) <= FP32_TOL
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("d,m,stride,arctan,k0,w", [
+    (1_048_576, 512, 1, False, 700_000, 256),      # BASELINE config 4
+    (2_097_152, 128, 4, True, 1_500_000, 1024),    # BASELINE config 5 (arctan, stride 4)
+])
+def test_cfg4_cfg5_full_size_window_vs_port(capi, port, d, m, stride, arctan, k0, w):
+    """Configs 4 and 5 at full size on one GPU, a window checked against the C
+    restatement (config 5's arctan operator is the north-star extension)."""
+    g = np.random.default_rng(d + m)
+    x = g.standard_normal((m, d), dtype=np.float32).astype(np.float64)
+    idx = None if stride <= 1 else np.arange(0, d, stride, dtype=np.int64)
+    y = g.standard_normal(d if idx is None else idx.size, dtype=np.float32).astype(np.float64)
+    got = capi.analyze_host(x, y, 1.0, idx, arctan=arctan)
+    assert np.isfinite(got).all()
+    if idx is None:
+        yw, iw = y[k0:k0 + w], None
+    else:
+        sel = (idx >= k0) & (idx < k0 + w)
+        yw, iw = y[sel], idx[sel]
+    want = port.analyze(x[:, k0:k0 + w], yw, 1.0, iw, k0=k0, d_total=d, arctan=arctan)
+    assert rel_l2(got[:, k0:k0 + w], want) <= FP32_TOL
+
+
 # --- extension: arctan observation operator (north_star, configs 1 and 5) ---
 # No reference implementation exists (proj/include/turbda/observation.hpp:12
 # has identity and index_selection only): the oracle is the C restatement
