@@ -194,9 +194,12 @@ TURBDA_API int turbda_diag(const double* members, int32_t n_members, int64_t d, 
 
 /*
  * NCCL communicator for state-dimension sharding across processes (one rank
- * per GPU).  Only the joint score mode exchanges data; the componentwise
- * mode never needs it.  NCCL is loaded on first use (dlopen("libnccl.so.2"),
- * the copy torch already loaded when present).
+ * per GPU).  The joint score mode exchanges the per-step distances through
+ * it; the componentwise mode needs none, but with a communicator a window
+ * (d_local < d_total) min-reduces its divergence verdict, so every rank
+ * reports the unsharded run's SamplerDivergedError, and turbda_diag sums
+ * its partials over the ranks.  NCCL is loaded on first use
+ * (dlopen("libnccl.so.2"), the copy torch already loaded when present).
  *   rank 0: turbda_comm_unique_id(id) -> broadcast the 128 bytes -> every
  *   rank: turbda_comm_init(device, rank, world, id).
  */

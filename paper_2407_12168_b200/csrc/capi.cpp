@@ -335,6 +335,9 @@ int ws_streams(Workspace* w, int n, turbda_status* st) {
     return TURBDA_OK;
 }
 
+int reduce_verdict_across_ranks(const turbda_ensf_params* p, Workspace* w,
+                                unsigned long long* dstatus, cudaStream_t s, turbda_status* st);
+
 // Runs one analysis slice on one device.  Host mode: `forecast`/`out` are the
 // call's host arrays with row pitch p->d_local (or member rows); the slice
 // starts at column win.k0_local.  The slice is cut into up to kMaxChunks (32)
@@ -522,6 +525,7 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
     w->last_eps = p->eps;
 
     if (on_dev && (p->flags & TURBDA_ASYNC)) {
+        if (int rc = reduce_verdict_across_ranks(p, w, dstatus, s, st)) return rc;
         TB_CUDA(ws_release(w, s, true));
         return TURBDA_OK;
     }
@@ -551,6 +555,8 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
             TB_CUDA(cudaStreamWaitEvent(s, w->ev_chunk[size_t(q)], 0));
         }
     }
+    // every chunk stream has been joined into s: the verdict is final here
+    if (int rc = reduce_verdict_across_ranks(p, w, dstatus, s, st)) return rc;
     TB_CUDA(cudaMemcpyAsync(w->status_host, dstatus, sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, s));
     TB_CUDA(cudaStreamSynchronize(s));
@@ -593,6 +599,21 @@ NcclApi* nccl_api() {
 
 int nccl_fail(turbda_status* st, NcclApi* api, ncclResult_t r, const char* where) {
     return fail(st, TURBDA_CUDA, std::string(where) + ": " + (api ? api->error_string(r) : "nccl"));
+}
+
+// A window of a state sharded over ranks that share a communicator
+// (turbda_comm_init): the divergence verdict is min-reduced over the ranks,
+// so every rank reports the globally first (particle, step) - the error the
+// unsharded reference run raises.
+int reduce_verdict_across_ranks(const turbda_ensf_params* p, Workspace* w,
+                                unsigned long long* dstatus, cudaStream_t s, turbda_status* st) {
+    if (!w->comm || w->comm_world <= 1 || p->d_local >= p->d_total) return TURBDA_OK;
+    NcclApi* api = nccl_api();
+    if (!api) return fail(st, TURBDA_CUDA, "libnccl.so.2 not loadable");
+    const ncclResult_t r = api->all_reduce(dstatus, dstatus, 1, ncclUint64, ncclMin,
+                                           static_cast<ncclComm_t>(w->comm), s);
+    if (r != ncclSuccess) return nccl_fail(st, api, r, "ncclAllReduce(verdict)");
+    return TURBDA_OK;
 }
 
 // In-process cliques for device_count > 1 joint runs: comms[g] for device dev0 + g.
@@ -1061,6 +1082,14 @@ int turbda_diag(const double* members, int32_t m, int64_t d, const double* truth
     }
     TB_CUDA(launch_diag(dx, m, d, dt, dsum, s));
     ++g_launches;
+    if (w->comm && w->comm_world > 1) {
+        // a state sharded over the communicator's ranks: global partial sums
+        NcclApi* api = nccl_api();
+        if (!api) return fail(st, TURBDA_CUDA, "libnccl.so.2 not loadable");
+        const ncclResult_t r = api->all_reduce(dsum, dsum, 2, ncclDouble, ncclSum,
+                                               static_cast<ncclComm_t>(w->comm), s);
+        if (r != ncclSuccess) return nccl_fail(st, api, r, "ncclAllReduce(diag)");
+    }
     TB_CUDA(cudaMemcpyAsync(out, dsum, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     TB_CUDA(cudaStreamSynchronize(s));
     TB_CUDA(ws_release(w, s, false));

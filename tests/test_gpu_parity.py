@@ -380,6 +380,7 @@ def test_joint_mode_multi_process_nccl(capi):
            str(ROOT / "tools" / "joint_multiproc_check.py")]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert "JOINT_MULTIPROC_OK" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "SHARD_VERDICT_OK" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
 
 
 def test_async_calls_on_two_streams_do_not_share_scratch(capi):

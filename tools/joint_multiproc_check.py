@@ -1,10 +1,13 @@
-"""Multi-process joint-norm check (run under torchrun, one rank per GPU).
+"""Multi-process sharding check (run under torchrun, one rank per GPU).
 
 Each rank analyses its contiguous shard of a d-coordinate state with the joint
 score; the library's NCCL communicator (turbda_comm_init) sums the per-step
 N x N (+2N) distance partials - the one collective of the path.  Rank 0
 gathers the shards and compares with the C oracle on the whole state, and
 checks the componentwise mode reassembles bit-exactly with no collective.
+With the communicator the componentwise shards also min-reduce their
+divergence verdict (every rank raises the unsharded run's error) and
+turbda_diag sums the rmse/spread partials over the shards.
 
     torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/joint_multiproc_check.py
 """
@@ -54,6 +57,33 @@ def main():
               f"{np.array_equal(got_c, whole_c)}", flush=True)
         ok = ej <= 1e-9 and np.array_equal(got_c, whole_c)
         print("JOINT_MULTIPROC_OK" if ok else "JOINT_MULTIPROC_FAIL", flush=True)
+    # divergence only inside the last rank's window: every rank must report
+    # the unsharded run's (particle, step)
+    r = np.ones(d)
+    r[d * (world - 1) // world + 7] = 1e-9
+    verdict = None
+    try:
+        capi.analyze_host(x[:, lo:hi], y[lo:hi], r[lo:hi], None, n_steps=20, device=local,
+                          k0=lo, d_total=d, precision=capi.FP64)
+    except capi.TurbdaError as e:
+        verdict = (e.code, e.diverged_particle, e.diverged_step)
+    verdicts = [None] * world
+    dist.all_gather_object(verdicts, verdict)
+    # rmse / spread partial sums over the shards
+    truth = y
+    sums = capi.diag(x[:, lo:hi], truth[lo:hi], device=local)
+    if rank == 0:
+        whole = None
+        try:
+            capi.analyze_host(x, y, r, None, n_steps=20, device=local, precision=capi.FP64)
+        except capi.TurbdaError as e:
+            whole = (e.code, e.diverged_particle, e.diverged_step)
+        mean = x.mean(axis=0)
+        want = (float(((mean - truth) ** 2).sum()), float(((x - mean) ** 2).sum()))
+        ok_v = whole is not None and whole[0] == capi.DIVERGED and all(v == whole for v in verdicts)
+        ok_d = all(abs(a - b) <= 1e-10 * abs(b) for a, b in zip(sums, want))
+        print(f"verdicts {verdicts} whole {whole}; diag {sums} want {want}", flush=True)
+        print("SHARD_VERDICT_OK" if ok_v and ok_d else "SHARD_VERDICT_FAIL", flush=True)
     capi.comm_destroy(local)
     dist.barrier()
     dist.destroy_process_group()
