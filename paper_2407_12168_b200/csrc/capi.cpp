@@ -755,6 +755,7 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
     }
     TB_CUDA(launch_relax_f64(z, dx, m, dl, p->relax_factor, dout, s));
     g_launches += 3 + 4 * uint64_t(p->n_steps);
+    if (int rc = reduce_verdict_across_ranks(p, w, dstatus, s, st)) return rc;
     if (on_dev && (p->flags & TURBDA_ASYNC)) {
         TB_CUDA(ws_release(w, s, true));
         return TURBDA_OK;
