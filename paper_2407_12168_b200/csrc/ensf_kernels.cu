@@ -109,7 +109,7 @@ __device__ __forceinline__ float2 ex2_poly2(float2 e) {
 // u_j falls with x_j (alpha > 0), so the nearest member sits where u changes
 // sign.  All 2P searches of a thread (P particles x the coordinate pair)
 // advance together, so each probe round issues 2P independent LDS and the
-// shared-memory latency overlaps; ceil(log2(J + 1)) rounds replace a pass
+// shared-memory latency overlaps; ceil(log2 J) rounds replace a pass
 // over all J members.
 template <int P>
 __device__ __forceinline__ void nearest_abs_u(const float* __restrict__ xsf, int lane, int j_n,
@@ -154,8 +154,8 @@ __device__ __forceinline__ float sort_key(float v) { return v != v ? __int_as_fl
 // kPolyEvery: every kPolyEvery-th (member, particle) slot of the unrolled
 // member loop takes its two exponentials from ex2_poly2 instead of MUFU.
 template <int P, bool kMinibatch, bool kSorted, int kPolyEvery, int kMinBlocks = 1,
-          bool kGlobalX = false>
-__global__ void __launch_bounds__(256, kMinBlocks) ensf_f32_kernel(KernelArgs a, const float* __restrict__ xt,
+          bool kGlobalX = false, int kThreads = 256>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelArgs a, const float* __restrict__ xt,
                                                        const double2* __restrict__ ab,
                                                        const StepF32* __restrict__ steps,
                                                        const int32_t* __restrict__ batches,
@@ -210,7 +210,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) ensf_f32_kernel(KernelArgs a,
     const float2 nA2 = make_float2(-A2.x, -A2.y);
     const bool has_y = kl + 1 < a.dl;  // the pair's second coordinate is real
     int top = 1;
-    while (top * 2 <= a.j_batch) top *= 2;
+    // probes top, top/2, .., 1 reach pos <= 2 top - 1 >= J - 1; pos = J - 1
+    // when all J members have u > 0 still yields the right pair (J-2, J-1)
+    while (top * 2 < a.j_batch) top *= 2;
     mbar_wait(&tile_bar, 0);  // step table and member tile have landed
 
     const int i0 = (blockIdx.y * nwarps + warp) * P;
@@ -650,7 +652,13 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
                          unsigned long long* status, cudaStream_t st, bool sorted) {
     // warps per CTA: enough to cover the members, at most 8
     const int groups = (a.m + P - 1) / P;
-    const int nw = groups < 8 ? groups : 8;
+    static const int ctas_env = [] {
+        const char* e = std::getenv("TURBDA_F32_CTAS");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int ctas = ctas_env ? ctas_env : (sorted ? 3 : 4);
+    const int wmax = (sorted && ctas == 7) ? 4 : 8;
+    const int nw = groups < wmax ? groups : wmax;
     const dim3 block(32 * nw);
     const dim3 grid(unsigned((a.dl + kTile - 1) / kTile), unsigned((groups + nw - 1) / nw));
     const bool global_x = f32_members_global(a.m, a.n_steps);
@@ -662,11 +670,6 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
     // (3 CTAs of 256 threads per SM), the brute-force-shift kernel (N <= 24,
     // fewer warps per CTA) at 64 (measured, tools/sweep_ctas.sh: config 3
     // -2.7 %); TURBDA_F32_CTAS=3|4 overrides for experiments
-    static const int ctas_env = [] {
-        const char* e = std::getenv("TURBDA_F32_CTAS");
-        return e ? std::atoi(e) : 0;
-    }();
-    const int ctas = ctas_env ? ctas_env : (sorted ? 3 : 4);
     auto kern = global_x ? (a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3, true>
                                         : ensf_f32_kernel<P, false, false, 0, 3, true>)
                 : a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3>
@@ -674,6 +677,8 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
                                          : ensf_f32_kernel<P, false, false, 0, 3>)
                 : variant == 1 ? ensf_f32_kernel<P, false, true, 8, 3>
                 : ctas == 4    ? ensf_f32_kernel<P, false, true, 0, 4>
+                : ctas == 7    ? ensf_f32_kernel<P, false, true, 0, 7, false, 128>
+                : ctas == 2    ? ensf_f32_kernel<P, false, true, 0, 2>
                                : ensf_f32_kernel<P, false, true, 0, 3>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
