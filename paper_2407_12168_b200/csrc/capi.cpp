@@ -372,14 +372,22 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
     if (j_batch != m)
         if (int rc = upload_batches(w, p, j_batch, s, st)) return rc;
 
-    // chunking (host mode): >= 8 MB of forecast per chunk, tile aligned
+    // chunking (host mode): >= 2 MB of forecast per chunk (at most
+    // kMaxChunks), tile aligned; smaller chunks expose less of the first
+    // H2D and the last D2H (config 2 e2e: 14.82 ms at 2 MB, 14.94 at 8 MB,
+    // 16.80 unchunked; tools/sweep_chunks.sh)
     std::vector<Window> chunks;
     {
         const int64_t tiles = (dl + 63) / 64;
         int c = 1;
         if (!on_dev) {
             const int64_t bytes = int64_t(md) * int64_t(sizeof(double));
-            c = int(std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, bytes / (8 << 20))));
+            static const int64_t chunk_bytes = [] {
+                const char* e = std::getenv("TURBDA_CHUNK_MB");
+                const int64_t mb = e ? std::atoll(e) : 0;
+                return (mb > 0 ? mb : 2) << 20;
+            }();
+            c = int(std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, bytes / chunk_bytes)));
             c = int(std::min<int64_t>(c, std::max<int64_t>(tiles, 1)));
         }
         int64_t start = 0;
