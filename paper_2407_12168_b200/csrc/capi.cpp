@@ -512,7 +512,7 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
             float* zc = w->z.as<float>() + moff;
             TB_CUDA(launch_ensf_f32(a, dx, abc, w->steps.as<StepF32>(), w->batches.as<int32_t>(),
                                     reinterpret_cast<float*>(w->xt.as<unsigned char>() + xt_off[size_t(q)]),
-                                    zc, dstatus, cs));
+                                    zc, dstatus, cs, dl));
             if (prof.b) TB_CUDA(cudaEventRecord(prof.b, cs));
             TB_CUDA(launch_relax_f32(zc, dx, m, c.dl, p->relax_factor, dout, cs));
         } else {

@@ -61,9 +61,13 @@ cudaError_t launch_obs_prep(const double* y, const double* r, const int64_t* idx
 // first converts (and, without minibatches, sorts per coordinate) the
 // forecast into fp32 tiles `xt` of ensf_f32_scratch_bytes(m, dl) bytes.
 size_t ensf_f32_scratch_bytes(int m, int64_t dl);
+// dl_concurrent: coordinates analysed concurrently with this launch (the
+// whole call when the host pipeline runs chunks side by side; 0 = a.dl),
+// which sets the particles-per-warp choice.
 cudaError_t launch_ensf_f32(const KernelArgs& a, const double* x, const double2* ab,
                             const StepF32* steps, const int32_t* batches, float* xt, float* z,
-                            unsigned long long* status, cudaStream_t st);
+                            unsigned long long* status, cudaStream_t st,
+                            int64_t dl_concurrent = 0);
 cudaError_t launch_ensf_f64(const KernelArgs& a, const double* x, const double2* ab,
                             const StepF64* steps, const int32_t* batches, double* z,
                             unsigned long long* status, cudaStream_t st);

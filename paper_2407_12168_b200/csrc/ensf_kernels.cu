@@ -732,7 +732,7 @@ size_t ensf_f32_scratch_bytes(int m, int64_t dl) {
 
 cudaError_t launch_ensf_f32(const KernelArgs& a, const double* x, const double2* ab,
                             const StepF32* steps, const int32_t* batches, float* xt, float* z,
-                            unsigned long long* status, cudaStream_t st) {
+                            unsigned long long* status, cudaStream_t st, int64_t dl_concurrent) {
     if (a.dl <= 0) return cudaSuccess;
     const unsigned tiles = unsigned((a.dl + kTile - 1) / kTile);
     // sorted tiles + binary-searched shift pay off past ~24 members; below,
@@ -755,7 +755,7 @@ cudaError_t launch_ensf_f32(const KernelArgs& a, const double* x, const double2*
     if (e != cudaSuccess) return e;
     // particles per warp: 4 when the grid still fills the GPU (a full wave
     // is 148 SMs x 24 warps), fewer for small windows so more warps exist
-    const int64_t tiles_n = (a.dl + kTile - 1) / kTile;
+    const int64_t tiles_n = (std::max(a.dl, dl_concurrent) + kTile - 1) / kTile;
     const auto warps_for = [&](int pp) { return tiles_n * ((a.m + pp - 1) / pp); };
     const int64_t wave = 148 * 24;
     // (particles past m in the last warp are computed and discarded)
