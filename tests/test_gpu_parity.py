@@ -196,6 +196,27 @@ def test_device_pointer_path_matches_host_path(capi):
     assert np.array_equal(out.cpu().numpy(), host)
 
 
+@pytest.mark.parametrize("d,stride", [(65536, 4), (65536 + 37, 1)])
+def test_chunked_host_pipeline_matches_device_path(capi, d, stride):
+    """Host buffers of 32 MB run as 16 concurrent 2 MB chunks (tile-aligned
+    coordinate ranges on their own streams); the result is bit-identical to
+    one device-pointer launch over the whole window."""
+    torch = pytest.importorskip("torch")
+    x, y, idx = throughput_inputs(64, d, stride=stride)
+    host = capi.analyze_host(x, y, 1.0, idx, n_steps=20)
+    dev = torch.device("cuda:0")
+    tx = torch.from_numpy(x).to(dev)
+    ty = torch.from_numpy(y).to(dev)
+    tr = torch.ones_like(ty)
+    ti = None if idx is None else torch.from_numpy(idx).to(dev)
+    out = torch.empty_like(tx)
+    p = capi.params(d_total=d, d_local=d, obs_dim=y.size, n_members=64, n_steps=20,
+                    obs_kind=0 if idx is None else 1, device=0, flags=capi.INPUTS_ON_DEVICE)
+    capi.analyze(p, tx, ty, tr, ti, out, stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), host)
+
+
 @pytest.mark.parametrize("precision,stride,joint", [(0, 1, False), (0, 4, False), (1, 4, False),
                                                     (1, 1, True)])
 def test_uniform_r_flag_matches_r_array(capi, precision, stride, joint):
