@@ -154,7 +154,7 @@ __device__ __forceinline__ float sort_key(float v) { return v != v ? __int_as_fl
 // kPolyEvery: every kPolyEvery-th (member, particle) slot of the unrolled
 // member loop takes its two exponentials from ex2_poly2 instead of MUFU.
 template <int P, bool kMinibatch, bool kSorted, int kPolyEvery, int kMinBlocks = 1,
-          bool kGlobalX = false, int kThreads = 256>
+          bool kGlobalX = false, int kThreads = 256, bool kShiftFree = true>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelArgs a, const float* __restrict__ xt,
                                                        const double2* __restrict__ ab,
                                                        const StepF32* __restrict__ steps,
@@ -232,69 +232,106 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
         const int32_t* bt = kMinibatch ? batches + size_t(s) * size_t(a.j_batch) : nullptr;
 
         // u_j = s (z - alpha x_j): one FFMA2 per member and coordinate pair
-        float2 zs[P], mn[P];
+        float2 zs[P];
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-            zs[p] = __fmul2_rn(z[p], f2(c.s));
-            mn[p] = f2(FLT_MAX);
-        }
-        // pass 1: per-coordinate smallest |u| (the softmax shift of
-        // proj/src/ensf.cpp:41-50, taken on |u| so no square is needed)
-        if (kSorted) {
-            nearest_abs_u<P>(xsf, lane, a.j_batch, top, c.nas, zs, mn);
-        } else {
-#pragma unroll 4
-            for (int jj = 0; jj < a.j_batch; ++jj) {
+        for (int p = 0; p < P; ++p) zs[p] = __fmul2_rn(z[p], f2(c.s));
+
+        // pass 2: w = 2^(c - u^2); den = sum w; num = sum w u,
+        // proj/src/ensf.cpp:51-61 in the cancellation-free form of :62-63
+        // (any shift c cancels in num / den)
+        auto weight_pass = [&](const float2 (&m2)[P], float2 (&den)[P], float2 (&num)[P]) {
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                den[p] = f2(0.f);
+                num[p] = f2(0.f);
+            }
+            int jj = 0;
+            for (; jj + U <= a.j_batch; jj += U) {
+#pragma unroll
+                for (int uu = 0; uu < U; ++uu) {
+                    const int j = kMinibatch ? __ldg(bt + jj + uu) : jj + uu;
+                    const float2 xv = kGlobalX ? __ldg(xs + j * 32 + lane) : xs[j * 32 + lane];
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        const float2 u = __ffma2_rn(nas2, xv, zs[p]);
+                        const float2 e = __ffma2_rn(make_float2(-u.x, -u.y), u, m2[p]);
+                        float2 w;
+                        if (kPolyEvery > 0 && (uu * P + p) % kPolyEvery == kPolyEvery - 1)
+                            w = ex2_poly2(e);
+                        else
+                            w = make_float2(ex2f(e.x), ex2f(e.y));
+                        den[p] = __fadd2_rn(den[p], w);
+                        num[p] = __ffma2_rn(w, u, num[p]);
+                    }
+                }
+            }
+            for (; jj < a.j_batch; ++jj) {
                 const int j = kMinibatch ? __ldg(bt + jj) : jj;
                 const float2 xv = kGlobalX ? __ldg(xs + j * 32 + lane) : xs[j * 32 + lane];
 #pragma unroll
                 for (int p = 0; p < P; ++p) {
                     const float2 u = __ffma2_rn(nas2, xv, zs[p]);
-                    mn[p].x = fminf(mn[p].x, fabsf(u.x));
-                    mn[p].y = fminf(mn[p].y, fabsf(u.y));
-                }
-            }
-        }
-        // pass 2: w = 2^(min u^2 - u^2); den = sum w; num = sum w u,
-        // proj/src/ensf.cpp:51-61 in the cancellation-free form of :62-63
-        float2 m2[P], den[P], num[P];
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-            m2[p] = __fmul2_rn(mn[p], mn[p]);
-            den[p] = f2(0.f);
-            num[p] = f2(0.f);
-        }
-        int jj = 0;
-        for (; jj + U <= a.j_batch; jj += U) {
-#pragma unroll
-            for (int uu = 0; uu < U; ++uu) {
-                const int j = kMinibatch ? __ldg(bt + jj + uu) : jj + uu;
-                const float2 xv = kGlobalX ? __ldg(xs + j * 32 + lane) : xs[j * 32 + lane];
-#pragma unroll
-                for (int p = 0; p < P; ++p) {
-                    const float2 u = __ffma2_rn(nas2, xv, zs[p]);
                     const float2 e = __ffma2_rn(make_float2(-u.x, -u.y), u, m2[p]);
-                    float2 w;
-                    if (kPolyEvery > 0 && (uu * P + p) % kPolyEvery == kPolyEvery - 1)
-                        w = ex2_poly2(e);
-                    else
-                        w = make_float2(ex2f(e.x), ex2f(e.y));
+                    const float2 w = make_float2(ex2f(e.x), ex2f(e.y));
                     den[p] = __fadd2_rn(den[p], w);
                     num[p] = __ffma2_rn(w, u, num[p]);
                 }
             }
-        }
-        for (; jj < a.j_batch; ++jj) {
-            const int j = kMinibatch ? __ldg(bt + jj) : jj;
-            const float2 xv = kGlobalX ? __ldg(xs + j * 32 + lane) : xs[j * 32 + lane];
+        };
+        // pass 1: per-coordinate smallest |u| (the softmax shift of
+        // proj/src/ensf.cpp:41-50, taken on |u| so no square is needed)
+        auto nearest_pass = [&](float2 (&m2)[P]) {
+            float2 mn[P];
+#pragma unroll
+            for (int p = 0; p < P; ++p) mn[p] = f2(FLT_MAX);
+            if (kSorted) {
+                nearest_abs_u<P>(xsf, lane, a.j_batch, top, c.nas, zs, mn);
+            } else {
+#pragma unroll 4
+                for (int jj = 0; jj < a.j_batch; ++jj) {
+                    const int j = kMinibatch ? __ldg(bt + jj) : jj;
+                    const float2 xv = kGlobalX ? __ldg(xs + j * 32 + lane) : xs[j * 32 + lane];
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        const float2 u = __ffma2_rn(nas2, xv, zs[p]);
+                        mn[p].x = fminf(mn[p].x, fabsf(u.x));
+                        mn[p].y = fminf(mn[p].y, fabsf(u.y));
+                    }
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < P; ++p) m2[p] = __fmul2_rn(mn[p], mn[p]);
+        };
+
+        float2 m2[P], den[P], num[P];
+        if (kShiftFree) {
+            // shift c = 0: w = 2^(-u^2) is exact to fp32 rounding while the
+            // nearest member has min u^2 <= 60 (then den >= 2^-min >= 2^-60
+            // and nothing that matters reaches the 2^-126 flush).  Values with
+            // den < 2^-60 (or NaN) are redone with the exact shift; the choice
+            // is per value, so results do not depend on the warp's other lanes.
+#pragma unroll
+            for (int p = 0; p < P; ++p) m2[p] = f2(0.f);
+            weight_pass(m2, den, num);
+            unsigned redo = 0;
 #pragma unroll
             for (int p = 0; p < P; ++p) {
-                const float2 u = __ffma2_rn(nas2, xv, zs[p]);
-                const float2 e = __ffma2_rn(make_float2(-u.x, -u.y), u, m2[p]);
-                const float2 w = make_float2(ex2f(e.x), ex2f(e.y));
-                den[p] = __fadd2_rn(den[p], w);
-                num[p] = __ffma2_rn(w, u, num[p]);
+                if (!(den[p].x >= 0x1.0p-60f)) redo |= 1u << (2 * p);
+                if (!(den[p].y >= 0x1.0p-60f)) redo |= 2u << (2 * p);
             }
+            if (__any_sync(0xffffffffu, redo != 0)) {
+                // the other values keep c = 0 and recompute the same bits
+                nearest_pass(m2);
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    if (!(redo & (1u << (2 * p)))) m2[p].x = 0.f;
+                    if (!(redo & (2u << (2 * p)))) m2[p].y = 0.f;
+                }
+                weight_pass(m2, den, num);
+            }
+        } else {
+            nearest_pass(m2);
+            weight_pass(m2, den, num);
         }
         // posterior score + Euler-Maruyama, proj/src/ensf.cpp:197-214
         const uint64_t n0 = uint64_t(s + 1) * uint64_t(a.d_total) + kg;
@@ -673,9 +710,11 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
     auto kern = global_x ? (a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3, true>
                                         : ensf_f32_kernel<P, false, false, 0, 3, true>)
                 : a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3>
-                : !sorted   ? (ctas == 4 ? ensf_f32_kernel<P, false, false, 0, 4>
-                                         : ensf_f32_kernel<P, false, false, 0, 3>)
+                : !sorted   ? (variant == 6 ? ensf_f32_kernel<P, false, false, 0, 4, false, 256, false>
+                               : ctas == 4  ? ensf_f32_kernel<P, false, false, 0, 4>
+                                            : ensf_f32_kernel<P, false, false, 0, 3>)
                 : variant == 1 ? ensf_f32_kernel<P, false, true, 8, 3>
+                : variant == 5 ? ensf_f32_kernel<P, false, true, 0, 3, false, 256, false>
                 : ctas == 4    ? ensf_f32_kernel<P, false, true, 0, 4>
                 : ctas == 7    ? ensf_f32_kernel<P, false, true, 0, 7, false, 128>
                 : ctas == 2    ? ensf_f32_kernel<P, false, true, 0, 2>

@@ -6,6 +6,7 @@ Tolerances (stated per BASELINE.md section 5 / SURVEY.md 8(c)):
 Sharding / determinism properties are bit-exact.
 """
 import numpy as np
+from pathlib import Path
 import pytest
 
 from conftest import ROOT, case_kwargs, load_cases
@@ -194,6 +195,52 @@ def test_device_pointer_path_matches_host_path(capi):
     capi.analyze(p, tx, ty, tr, ti, out, stream=torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), host)
+
+
+@pytest.mark.parametrize("m,minibatch,y0,r", [(16, 0, 30.0, 0.2), (16, 0, 50.0, 0.5),
+                                               (48, 0, 30.0, 0.2), (48, 0, 50.0, 0.5),
+                                               (48, 20, 50.0, 0.5)])
+def test_far_from_members_exact_shift_redo(capi, port, m, minibatch, y0, r):
+    """The fp32 weight pass runs without a shift (w = 2^-u^2) and redoes a
+    value with the exact shift of proj/src/ensf.cpp:41-50 when its nearest
+    member is far (den < 2^-60).  Tight members (spread 0.05) and strong
+    observations far away put the late-step particles there: min u^2 > 60
+    for every value at y = 30, r = 0.2 and for ~58 % at y = 50, r = 0.5 (so
+    both paths meet inside one warp) — sorted (N = 48), brute-force (N = 16)
+    and minibatch member loops against the C oracle."""
+    g = np.random.default_rng(5)
+    d = 256
+    x = (0.05 * g.standard_normal((m, d))).astype(np.float32).astype(np.float64)
+    y = np.full(d, y0)
+    want = port.analyze(x, y, r, n_steps=100, minibatch_j=minibatch, relax_factor=0.0)
+    got = capi.analyze_host(x, y, r, n_steps=100, minibatch_j=minibatch, relax_factor=0.0,
+                            precision=capi.FP32)
+    assert rel_l2(got, want) <= FP32_TOL, rel_l2(got, want)
+
+
+def test_shift_free_weights_match_exact_shift_kernel(capi, tmp_path):
+    """Default kernel (shift-free weight pass + per-value redo) vs the kernel
+    that always takes the exact shift first (TURBDA_F32_VARIANT=5 sorted,
+    =6 brute force; a fresh process, the variant is read once): the same
+    estimator to fp32 rounding."""
+    import os
+    import subprocess
+    import sys
+    for m, variant in ((64, 5), (20, 6)):
+        x, y, idx = throughput_inputs(m, 4096, stride=4)
+        np.save(tmp_path / "x.npy", x)
+        np.save(tmp_path / "y.npy", y)
+        np.save(tmp_path / "i.npy", idx)
+        code = ("import numpy as np, sys; from paper_2407_12168_b200 import capi; "
+                "d = sys.argv[1]; x, y, i = (np.load(d + f) for f in ('/x.npy', '/y.npy', '/i.npy')); "
+                "np.save(d + '/out.npy', capi.analyze_host(x, y, 1.0, i, n_steps=100))")
+        env = dict(os.environ, TURBDA_F32_VARIANT=str(variant))
+        subprocess.run([sys.executable, "-c", code, str(tmp_path)], check=True, env=env,
+                       cwd=str(Path(__file__).resolve().parents[1]))
+        exact = np.load(tmp_path / "out.npy")
+        got = capi.analyze_host(x, y, 1.0, idx, n_steps=100)
+        assert rel_l2(got, exact) <= 1e-5, (m, rel_l2(got, exact))
+        assert not np.array_equal(got, exact)  # the variant really ran
 
 
 @pytest.mark.parametrize("d,stride", [(65536, 4), (65536 + 37, 1)])
