@@ -702,18 +702,31 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
     const int variant = f32_variant();
     const size_t smem = sizeof(StepF32) * size_t(a.n_steps) +
                         (global_x ? 0 : sizeof(float2) * 32 * size_t(a.m));
-    // letting ptxas take more registers (1 CTA/SM) loses ~20%
-    // register budget: the sorted kernel (N > 24) runs best at 80 registers
-    // (3 CTAs of 256 threads per SM), the brute-force-shift kernel (N <= 24,
-    // fewer warps per CTA) at 64 (measured, tools/sweep_ctas.sh: config 3
-    // -2.7 %); TURBDA_F32_CTAS=3|4 overrides for experiments
+    // letting ptxas take more registers (1 CTA/SM) loses ~20%.
+    // Sorted tiles (N > 24): 4 CTAs of 256 threads per SM (64 registers) with
+    // one in eight exponentials on the FMA-pipe polynomial when four member
+    // tiles fit in shared memory (config 2 13.18 -> 12.47 ms, config 5
+    // 809 -> 752 ms; tools/variant_sweep.sh), else 3 CTAs all-MUFU (config 4,
+    // N = 512: shared memory allows one CTA per SM and the polynomial loses
+    // 13 %).  Brute-force shift (N <= 24): 4 CTAs, all-MUFU (config 3; the
+    // polynomial is neutral there).  TURBDA_F32_CTAS / TURBDA_F32_VARIANT
+    // override for experiments.
+    const bool sorted_fast = sorted && variant == 0 && ctas_env == 0 &&
+                             smem * 4 <= size_t(227) * 1024;
     auto kern = global_x ? (a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3, true>
                                         : ensf_f32_kernel<P, false, false, 0, 3, true>)
                 : a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3>
                 : !sorted   ? (variant == 6 ? ensf_f32_kernel<P, false, false, 0, 4, false, 256, false>
+                               : variant == 10 ? ensf_f32_kernel<P, false, false, 8, 4>
+                               : variant == 11 ? ensf_f32_kernel<P, false, false, 16, 4>
+                               : variant == 12 ? ensf_f32_kernel<P, false, false, 4, 4>
                                : ctas == 4  ? ensf_f32_kernel<P, false, false, 0, 4>
                                             : ensf_f32_kernel<P, false, false, 0, 3>)
+                : sorted_fast  ? ensf_f32_kernel<P, false, true, 8, 4>
                 : variant == 1 ? ensf_f32_kernel<P, false, true, 8, 3>
+                : variant == 7 ? ensf_f32_kernel<P, false, true, 16, 3>
+                : variant == 8 ? ensf_f32_kernel<P, false, true, 4, 3>
+                : variant == 9 ? ensf_f32_kernel<P, false, true, 8, 4>
                 : variant == 5 ? ensf_f32_kernel<P, false, true, 0, 3, false, 256, false>
                 : ctas == 4    ? ensf_f32_kernel<P, false, true, 0, 4>
                 : ctas == 7    ? ensf_f32_kernel<P, false, true, 0, 7, false, 128>
