@@ -436,7 +436,10 @@ def main():
             "bound": "sfu (MUFU.EX2, one exp per pair-eval)",
             "achieved": pair_evals / (kern_ms / 1e3), "unit": "pair-evals/s",
             "peak": mufu_peak, "frac": pair_evals / (kern_ms / 1e3) / mufu_peak,
-            "peak_source": "16 ex2/clk/SM measured x 148 SMs x sm_max_mhz"} if not joint else {
+            "peak_source": "16 ex2/clk/SM measured x 148 SMs x sm_max_mhz",
+            "note": "MUFU-only ceiling; for N > 24 (sorted member tiles, up to ~200 members) one "
+                    "pair-eval slot in eight takes its exponential from an FMA-pipe polynomial, "
+                    "so that kernel's own MUFU-bound ceiling is 8/7 of this peak"} if not joint else {
             "bound": "fp64 pipe (Gram + weighted sum: 2 DFMA per pair-eval)",
             "achieved": 4.0 * pair_evals / (kern_ms / 1e3) / 1e12, "unit": "TFLOP/s",
             "peak": fp64_peak, "frac": 4.0 * pair_evals / (kern_ms / 1e3) / 1e12 / fp64_peak,
