@@ -694,12 +694,16 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
         return e ? std::atoi(e) : 0;
     }();
     const int ctas = ctas_env ? ctas_env : (sorted ? 3 : 4);
-    const int wmax = (sorted && ctas == 7) ? 4 : 8;
+    const int variant = f32_variant();
+    // variants 13-15: wide CTAs (16 / 32 warps) for tiles whose shared memory
+    // allows only one CTA per SM (config 4)
+    const int wmax = (sorted && ctas == 7) ? 4
+                     : (sorted && (variant == 13 || variant == 15)) ? 16
+                     : (sorted && variant == 14) ? 32 : 8;
     const int nw = groups < wmax ? groups : wmax;
     const dim3 block(32 * nw);
     const dim3 grid(unsigned((a.dl + kTile - 1) / kTile), unsigned((groups + nw - 1) / nw));
     const bool global_x = f32_members_global(a.m, a.n_steps);
-    const int variant = f32_variant();
     const size_t smem = sizeof(StepF32) * size_t(a.n_steps) +
                         (global_x ? 0 : sizeof(float2) * 32 * size_t(a.m));
     // letting ptxas take more registers (1 CTA/SM) loses ~20%.
@@ -724,6 +728,9 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
                                             : ensf_f32_kernel<P, false, false, 0, 3>)
                 : sorted_fast  ? ensf_f32_kernel<P, false, true, 8, 4>
                 : variant == 1 ? ensf_f32_kernel<P, false, true, 8, 3>
+                : variant == 13 ? ensf_f32_kernel<P, false, true, 0, 1, false, 512>
+                : variant == 14 ? ensf_f32_kernel<P, false, true, 0, 1, false, 1024>
+                : variant == 15 ? ensf_f32_kernel<P, false, true, 8, 1, false, 512>
                 : variant == 7 ? ensf_f32_kernel<P, false, true, 16, 3>
                 : variant == 8 ? ensf_f32_kernel<P, false, true, 4, 3>
                 : variant == 9 ? ensf_f32_kernel<P, false, true, 8, 4>
