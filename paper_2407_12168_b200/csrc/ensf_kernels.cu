@@ -694,25 +694,32 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
         return e ? std::atoi(e) : 0;
     }();
     const int ctas = ctas_env ? ctas_env : (sorted ? 3 : 4);
-    const int variant = f32_variant();
-    // variants 13-15: wide CTAs (16 / 32 warps) for tiles whose shared memory
-    // allows only one CTA per SM (config 4)
-    const int wmax = (sorted && ctas == 7) ? 4
-                     : (sorted && (variant == 13 || variant == 15)) ? 16
-                     : (sorted && variant == 14) ? 32 : 8;
-    const int nw = groups < wmax ? groups : wmax;
-    const dim3 block(32 * nw);
-    const dim3 grid(unsigned((a.dl + kTile - 1) / kTile), unsigned((groups + nw - 1) / nw));
     const bool global_x = f32_members_global(a.m, a.n_steps);
     const size_t smem = sizeof(StepF32) * size_t(a.n_steps) +
                         (global_x ? 0 : sizeof(float2) * 32 * size_t(a.m));
+    // variants 13-17: wide CTAs (16 / 32 warps) for tiles whose shared memory
+    // allows only one CTA per SM (config 4); the default picks kWideDefault there
+    constexpr int kWideDefault = 16;
+    const bool one_cta_per_sm = !global_x && smem * 2 > size_t(227) * 1024;
+    const int variant = (sorted && f32_variant() == 0 && ctas_env == 0 && one_cta_per_sm)
+                            ? kWideDefault : f32_variant();
+    const int wmax = (sorted && ctas == 7) ? 4
+                     : (sorted && (variant == 13 || variant == 15)) ? 16
+                     : (sorted && (variant == 14 || variant == 16)) ? 32
+                     : (sorted && variant == 17) ? 16 : 8;
+    const int nw = groups < wmax ? groups : wmax;
+    const dim3 block(32 * nw);
+    const dim3 grid(unsigned((a.dl + kTile - 1) / kTile), unsigned((groups + nw - 1) / nw));
     // letting ptxas take more registers (1 CTA/SM) loses ~20%.
     // Sorted tiles (N > 24): 4 CTAs of 256 threads per SM (64 registers) with
     // one in eight exponentials on the FMA-pipe polynomial when four member
     // tiles fit in shared memory (config 2 13.18 -> 12.47 ms, config 5
-    // 809 -> 752 ms; tools/variant_sweep.sh), else 3 CTAs all-MUFU (config 4,
-    // N = 512: shared memory allows one CTA per SM and the polynomial loses
-    // 13 %).  Brute-force shift (N <= 24): 4 CTAs, all-MUFU (config 3; the
+    // 809 -> 752 ms; tools/variant_sweep.sh).  When shared memory allows only
+    // one CTA per SM (config 4, N = 512: a 128 KB member tile) that CTA is
+    // 32 warps (64 registers) with the same one-in-eight polynomial share:
+    // config 4 6675 -> 5607 ms (8 warps all-MUFU 6675, 16 warps 6199,
+    // 32 warps 6169, 16 warps + 1/8 poly 5727, 16 warps + 1/4 poly 5990).
+    // Otherwise 3 CTAs all-MUFU.  Brute-force shift (N <= 24): 4 CTAs, all-MUFU (config 3; the
     // polynomial is neutral there).  TURBDA_F32_CTAS / TURBDA_F32_VARIANT
     // override for experiments.
     const bool sorted_fast = sorted && variant == 0 && ctas_env == 0 &&
@@ -731,6 +738,8 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
                 : variant == 13 ? ensf_f32_kernel<P, false, true, 0, 1, false, 512>
                 : variant == 14 ? ensf_f32_kernel<P, false, true, 0, 1, false, 1024>
                 : variant == 15 ? ensf_f32_kernel<P, false, true, 8, 1, false, 512>
+                : variant == 16 ? ensf_f32_kernel<P, false, true, 8, 1, false, 1024>
+                : variant == 17 ? ensf_f32_kernel<P, false, true, 4, 1, false, 512>
                 : variant == 7 ? ensf_f32_kernel<P, false, true, 16, 3>
                 : variant == 8 ? ensf_f32_kernel<P, false, true, 4, 3>
                 : variant == 9 ? ensf_f32_kernel<P, false, true, 8, 4>

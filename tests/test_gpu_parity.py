@@ -349,6 +349,20 @@ def test_cfg4_cfg5_full_size_window_vs_port(capi, port, d, m, stride, arctan, k0
     assert rel_l2(got[:, k0:k0 + w], want) <= FP32_TOL
 
 
+@pytest.mark.parametrize("m", [450, 512])
+def test_wide_cta_one_tile_per_sm_vs_port(capi, port, m):
+    """Ensembles whose member tile leaves room for one CTA per SM (N >= ~440)
+    run 32-warp CTAs with the polynomial share (config 4's path); ragged
+    particle groups (N = 450) and a ragged last tile (d = 130)."""
+    x, y, idx, _ = conditioned_inputs(m, 130, stride=3)
+    x = x.astype(np.float32).astype(np.float64)
+    y = y.astype(np.float32).astype(np.float64)
+    want = port.analyze(x, y, 0.5, idx, n_steps=20)
+    got = capi.analyze_host(x, y, 0.5, idx, n_steps=20)
+    assert np.isfinite(got).all()
+    assert rel_l2(got, want) <= FP32_TOL
+
+
 # --- extension: arctan observation operator (north_star, configs 1 and 5) ---
 # No reference implementation exists (proj/include/turbda/observation.hpp:12
 # has identity and index_selection only): the oracle is the C restatement
