@@ -2,29 +2,34 @@
 """EnSF analysis throughput on B200 (BASELINE.json metric: d x N x steps / s).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config cfg2|cfg1|cfg3|cfg4|cfg5] [--precision fp32|fp64]
-                    [--obs linear|arctan]
+                    [--config cfg3|cfg1|cfg2|cfg4|cfg5] [--precision fp32|fp64]
+                    [--score componentwise|joint] [--obs linear|arctan]
 
 One "step" is one full EnSF analysis (turbda::analyze: every pseudo-time
 step of the reverse SDE + relax_spread) of one synthetic forecast ensemble.
-Default workload: BASELINE config 2 (d = 131,072 coordinates per GPU, N = 64
-members, S = 100 pseudo-time steps, every-4th-point observations).  With
---gpus N (torchrun, one rank per GPU) every rank analyses its own
-131,072-coordinate shard of a d = 131,072 N state: weak scaling, no
-data-path collective (the componentwise score never couples coordinates);
-the barrier and the max-over-ranks of the device time are the only
-collectives.
+
+Default workload: BASELINE config 3, the configuration the metric is quoted
+on ("at 1/2/4/8 B200"): d = 16,777,216 coordinates (2048x2048x4) per GPU,
+N = 20 members, S = 100 pseudo-time steps, identity observations.  With
+--gpus N every rank analyses its own 16.8M-coordinate shard of a 16.8M x N
+state (weak scaling).  The componentwise score never couples coordinates,
+so there is no data-path collective: the barrier and the max-over-ranks of
+the device time are the only collectives.  Without an external launcher,
+``--gpus N`` (N > 1) re-launches itself under torch.distributed.run with N
+ranks (127.0.0.1 rendezvous); a line is printed only when the world size
+equals --gpus.
 
 Rank 0 prints ONE JSON line (keys per the driver contract).  The
 ``cpu_baseline`` leg and ``--impl reference`` time the reference's own CPU
 implementation (oracle/_ref: proj/src/ensf.cpp compiled unmodified) on this
-host's cores over a bounded coordinate sample of the same workload.
+host's cores over the same bounded coordinate sample of the workload.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -44,15 +49,17 @@ CONFIGS = {
     # name: (d per GPU, N, S, obs stride, description)
     "cfg1": (8192, 20, 50, 1, "BASELINE cfg1 shape: d=8192, N=20, S=50, identity obs"),
     "cfg2": (131072, 64, 100, 4, "BASELINE cfg2: d=131072 (256x256x2), N=64, S=100, every-4th-point obs"),
-    "cfg3": (16777216, 20, 100, 1, "BASELINE cfg3: d=16.8M (2048x2048x4), N=20, S=100"),
+    "cfg3": (16777216, 20, 100, 1, "BASELINE cfg3: d=16.8M (2048x2048x4) per GPU, N=20, S=100, identity obs"),
     "cfg4": (1048576, 512, 100, 1, "BASELINE cfg4: d=1M, N=512, S=100"),
     "cfg5": (2097152, 128, 100, 4, "BASELINE cfg5 analysis: d=2.1M (1024x1024x2), N=128, S=100, "
                                    "every-4th-point arctan obs"),
 }
+DEFAULT_CONFIG = "cfg3"
 # algorithmic bytes per unit for a per-step-streaming fp32
 # design (read z, read x, write z) - the HBM roofline the north star names.
 BYTES_PER_UNIT = 12
 MUFU_PER_CLK_PER_SM = 16  # ex2 throughput, measured (tools/pipe_microbench.cu)
+L2_BYTES = 126 * 2**20
 
 
 def peaks():
@@ -139,19 +146,40 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def make_inputs(d, m, stride, k0, seed=1234):
-    """Synthetic SQG-shaped forecast: N(0,1) members and observations (the
-    throughput generator of SURVEY.md 8(d), drawn with numpy here)."""
+def obs_layout(d, stride, k0):
+    """Observation indices of a shard: the global flat indices 0, s, 2s, ...
+    (make_grid_operator, proj/src/observation.cpp:29-41) inside [k0, k0+d)."""
+    if stride <= 1:
+        return None, d
+    first = (-k0) % stride
+    n = len(range(k0 + first, k0 + d, stride))
+    return (k0 + first, stride, n), n
+
+
+def make_inputs_host(d, m, stride, k0, seed=1234):
+    """Synthetic forecast for the CPU sample: N(0,1) members and observations
+    (the throughput generator of SURVEY.md 8(d); the timing is insensitive
+    to the values)."""
     rng = np.random.default_rng(seed + k0)
     x = rng.standard_normal((m, d))
-    if stride <= 1:
-        idx = None
-        y = rng.standard_normal(d)
-    else:
-        first = (-k0) % stride  # global indices 0, s, 2s, ... that fall in this shard
-        idx = np.arange(k0 + first, k0 + d, stride, dtype=np.int64)
-        y = rng.standard_normal(idx.size)
+    lay, nobs = obs_layout(d, stride, k0)
+    idx = None if lay is None else np.arange(lay[0], lay[0] + lay[1] * lay[2], lay[1],
+                                             dtype=np.int64)
+    y = rng.standard_normal(nobs)
     return x, y, idx
+
+
+def make_inputs_device(torch, dev, d, m, stride, k0, seed):
+    """The same synthetic shapes generated on the device (a 16.8M x 20
+    forecast is 2.7 GB: numpy would spend tens of seconds on it)."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed * 1000003 + k0)
+    x = torch.randn((m, d), generator=g, device=dev, dtype=torch.float64)
+    lay, nobs = obs_layout(d, stride, k0)
+    y = torch.randn((nobs,), generator=g, device=dev, dtype=torch.float64)
+    idx = None if lay is None else torch.arange(lay[0], lay[0] + lay[1] * lay[2], lay[1],
+                                                dtype=torch.int64, device=dev)
+    return x, y, torch.ones_like(y), idx
 
 
 def reference_rate(x, y, idx, n_steps, steps, warmup, arctan=False):
@@ -177,22 +205,32 @@ def reference_rate(x, y, idx, n_steps, steps, warmup, arctan=False):
         times.append(time.perf_counter() - t0)
     units = float(d) * m * n_steps
     total = sum(times)
+    fp_mb = x.nbytes / 1e6
     return {"value": units * steps / total, "unit": UNIT, "cores": min(cores, m),
             "threads_requested": cores, "kind": kind,
-            "sample": f"{m} members x {d} coordinates x {n_steps} pseudo-steps "
-                      f"(a {d}-coordinate slice of the workload), {steps} run(s), "
-                      f"median {statistics.median(times):.3f} s",
+            "sample": f"{m} members x {d} coordinates x {n_steps} pseudo-steps (a {d}-coordinate "
+                      f"slice of the workload; its {fp_mb:.0f} MB forecast is far more cache-"
+                      f"resident than the full state, which flatters the CPU), {warmup} warm-up + "
+                      f"{steps} timed run(s), median {statistics.median(times):.3f} s; the "
+                      f"reference parallelises over particles only, so at most N={m} threads",
             "ms_per_step": 1e3 * total / steps}
 
 
-def run_reference_arm(args, cfg, json_out=None):
-    """--impl reference: rank 0 times the reference's CPU implementation."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+def _cpu_sample(d, m, base):
+    """CPU sample width: `base` coordinates at N = 64, scaled by (64/N)^2 (the
+    CPU cost grows with N^2 per coordinate) so every config's CPU leg takes
+    seconds, a multiple of 64 coordinates."""
+    return max(64, min(d, int(base * (64.0 / m) ** 2) // 64 * 64))
+
+
+def run_reference_arm(args, json_out):
+    """--impl reference: rank 0 times the reference's CPU implementation on
+    the same config; other ranks exit without work."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    d_full, m, s, stride, desc = CONFIGS[cfg]
+    d_full, m, s, stride, desc = CONFIGS[args.config]
     d_sample = _cpu_sample(d_full, m, args.ref_sample_d)
-    x, y, idx = make_inputs(d_sample, m, stride, 0)
+    x, y, idx = make_inputs_host(d_sample, m, stride, 0)
     r = reference_rate(x, y, idx, s, args.steps, args.warmup, arctan=_arctan(args))
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
@@ -207,14 +245,7 @@ def run_reference_arm(args, cfg, json_out=None):
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), file=json_out or sys.stdout, flush=True)
-
-
-def _cpu_sample(d, m, base):
-    """CPU sample width: `base` coordinates at N = 64, scaled by (64/N)^2 (the
-    CPU cost grows with N^2 per coordinate) so every config's CPU leg takes
-    seconds, a multiple of 64 coordinates."""
-    return max(64, min(d, int(base * (64.0 / m) ** 2) // 64 * 64))
+    print(json.dumps(line), file=json_out, flush=True)
 
 
 def _arctan(args):
@@ -232,6 +263,33 @@ def _json_stdout():
     return out
 
 
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n):
+    """--gpus N without a launcher: one process per GPU under
+    torch.distributed.run (the driver's own launch line), stdout passed up."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    print(f"bench: spawning {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def timed_analyses(torch, fn, n, stream):
+    """Device time of n back-to-back calls on `stream` (CUDA events)."""
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for q in range(n):
+        fn(q)
+    b.record(stream)
+    b.synchronize()
+    return a.elapsed_time(b) / n
+
+
 def main():
     json_out = _json_stdout()
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
@@ -239,7 +297,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default=DEFAULT_CONFIG)
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--score", choices=["componentwise", "joint"], default="componentwise",
                     help="joint: the north-star joint-norm extension (fp64, one NCCL allreduce "
@@ -247,15 +305,21 @@ def main():
     ap.add_argument("--obs", choices=["linear", "arctan"], default=None,
                     help="observation operator (default: arctan for cfg5, linear otherwise)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-d", type=int, default=32768)
-    ap.add_argument("--ref-sample-d", type=int, default=8192)
+    ap.add_argument("--no-fp64", action="store_true", help="skip the fp64 faithful-path leg")
+    ap.add_argument("--no-e2e-variants", action="store_true",
+                    help="skip the pageable / C++ row-pointer end-to-end legs")
+    ap.add_argument("--ref-sample-d", type=int, default=8192,
+                    help="CPU sample width at N=64 (scaled by (64/N)^2); used by both the "
+                         "cpu_baseline leg and --impl reference")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
 
     if args.impl == "reference":
-        run_reference_arm(args, args.config, json_out)
+        run_reference_arm(args, json_out)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
 
     import torch
     import torch.distributed as dist
@@ -265,18 +329,24 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus and rank == 0:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if world != args.gpus:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE {world}: refusing to report",
+              file=sys.stderr)
+        sys.exit(2)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        if rank == 0:
+            print(f"bench: NCCL process group up, nranks={dist.get_world_size()}",
+                  file=sys.stderr, flush=True)
 
     d, m, s, stride, desc = CONFIGS[args.config]
     d_total = d * world
     k0 = rank * d
     joint = args.score == "joint"
     arctan = _arctan(args)
+    obs_kind = (0 if stride <= 1 else 1) + (2 if arctan else 0)
     # joint mode: distances/update in fp64 always; --precision picks the noise
     prec = capi.FP32 if args.precision == "fp32" else capi.FP64
     if joint and world > 1:
@@ -284,44 +354,38 @@ def main():
         dist.broadcast_object_list(uid, src=0)
         capi.comm_init(local, rank, world, uid[0])
 
-    # --- resident inputs: 3 rotating sets so the working set exceeds L2 ----
-    n_sets = 3
-    host_sets = [make_inputs(d, m, stride, k0, seed=1234 + 7 * q) for q in range(n_sets)]
-    dsets = []
-    for x, y, idx in host_sets:
-        tx = torch.from_numpy(x).to(dev)
-        ty = torch.from_numpy(y).to(dev)
-        tr = torch.ones_like(ty)
-        ti = None if idx is None else torch.from_numpy(idx).to(dev)
-        dsets.append((tx, ty, tr, ti))
+    # --- resident inputs -------------------------------------------------------
+    # working set > L2: one forecast of m*d*8 bytes per set; small workloads
+    # rotate 3 sets and flush L2 before every timed step
+    set_bytes = m * d * 8
+    n_sets = 1 if set_bytes > 4 * L2_BYTES else 3
+    dsets = [make_inputs_device(torch, dev, d, m, stride, k0, seed=1234 + 7 * q)
+             for q in range(n_sets)]
     out = torch.empty((m, d), dtype=torch.float64, device=dev)
-    obs_dim = host_sets[0][1].size
-    p = capi.params(d_total=d_total, k0=k0, d_local=d, obs_dim=obs_dim, n_members=m, n_steps=s,
-                    obs_kind=(0 if stride <= 1 else 1) + (2 if arctan else 0),
-                    precision=prec, device=local,
-                    flags=capi.INPUTS_ON_DEVICE | capi.ASYNC,
-                    score_mode=capi.SCORE_JOINT if joint else capi.SCORE_COMPONENTWISE)
+    obs_dim = dsets[0][1].numel()
+
+    def mkparams(precision, flags, cycle=1):
+        return capi.params(d_total=d_total, k0=k0, d_local=d, obs_dim=obs_dim, n_members=m,
+                           n_steps=s, obs_kind=obs_kind, precision=precision, device=local,
+                           flags=flags, cycle=cycle,
+                           score_mode=capi.SCORE_JOINT if joint else capi.SCORE_COMPONENTWISE)
+
+    p = mkparams(prec, capi.INPUTS_ON_DEVICE | capi.ASYNC)
     stream = torch.cuda.Stream(dev)  # a real stream: the events and kernels share it
     torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
 
-    def one(q):
+    def one(q, pp=p):
         tx, ty, tr, ti = dsets[q % n_sets]
-        capi.analyze(p, tx, ty, tr, ti, out, stream=sh)
+        capi.analyze(pp, tx, ty, tr, ti, out, stream=sh)
 
     for q in range(args.warmup):
         one(q)
     torch.cuda.synchronize(dev)
     capi.check(local, p)  # divergence verdict of the warm-up runs
 
-    # --- timed region: K device-resident analyses ---------------------------
-    # Inputs larger than L2 (3 rotating sets): the K steps are timed back to
-    # back.  Smaller workloads: L2 is flushed (a 512 MB write) before every
-    # step, outside that step's event pair, and the per-step times are summed.
-    l2_bytes = 126 * 2**20
-    set_bytes = n_sets * m * d * 8
-    # between two uses of one input set the other sets stream through L2
-    flush = (n_sets - 1) * m * d * 8 <= l2_bytes
+    # --- timed region: K device-resident analyses --------------------------------
+    flush = set_bytes * (n_sets - 1) <= L2_BYTES if n_sets > 1 else False
     scratch = torch.empty(512 * 2**20 // 4, dtype=torch.float32, device=dev) if flush else None
     capi.profile_enable(True)
     capi.profile_read()
@@ -363,49 +427,108 @@ def main():
     units_per_gpu = float(d) * m * s
     value = units_per_gpu * world / (ms / 1e3)
 
-    # --- end to end through the public API with pinned host buffers ---------
+    # --- fp64 faithful path, same config (device-resident, 1 warm-up + 2) -----
+    fp64 = None
+    if not args.no_fp64 and not joint and prec == capi.FP32:
+        p64 = mkparams(capi.FP64, capi.INPUTS_ON_DEVICE | capi.ASYNC)
+        one(0, p64)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        ms64 = timed_analyses(torch, lambda q: one(q, p64), 2, stream)
+        capi.check(local, p64)
+        t64 = torch.tensor([ms64], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t64, op=dist.ReduceOp.MAX)
+        fp64 = {"value": units_per_gpu * world / (float(t64[0]) / 1e3), "unit": UNIT,
+                "ms_per_step": float(t64[0]), "steps": 2, "warmup": 1,
+                "kernel": "ensf_f64_kernel (the reference's own fp64 arithmetic: "
+                          "fast_exp_nonpos, two-pass shift, num/den score)"}
+
+    # --- end to end through the public API with host buffers -------------------
     import paper_2407_12168_b200 as tb
     grid = tb.GridSpec()
     # any (nx, ny, nz=2) whose size is d: the API only checks the size
     grid.nz = 2
     grid.nx = 256 if d % 512 == 0 else d // 2
     grid.ny = d // (2 * grid.nx)
-    x0, y0, _ = host_sets[0]
-    hx = torch.from_numpy(x0).pin_memory().numpy()
-    hy_full = torch.from_numpy(np.ascontiguousarray(y0)).pin_memory().numpy()
-    hout = torch.empty((m, d), dtype=torch.float64).pin_memory().numpy()
-    e2e_times = []
-    if world > 1:
-        dist.barrier()
-    for q in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
+    tx0, ty0, _, ti0 = dsets[0]
+    hx = torch.empty((m, d), dtype=torch.float64, pin_memory=True)
+    hx.copy_(tx0)
+    hy = torch.empty((obs_dim,), dtype=torch.float64, pin_memory=True)
+    hy.copy_(ty0)
+    hx, hy = hx.numpy(), hy.numpy()
+    hidx = None if ti0 is None else ti0.cpu().numpy()
+    hout = torch.empty((m, d), dtype=torch.float64, pin_memory=True).numpy()
+    del dsets, out
+    torch.cuda.empty_cache()
+
+    def e2e_call(q, out_arr=hout, x_arr=hx, y_arr=hy):
         if joint and world > 1:
             # a window of the sharded state: the C-ABI with host buffers
-            pe = capi.params(d_total=d_total, k0=k0, d_local=d, obs_dim=obs_dim, n_members=m,
-                             n_steps=s, obs_kind=(0 if stride <= 1 else 1) + (2 if arctan else 0),
-                             precision=prec, device=local, cycle=1 + q,
-                             score_mode=capi.SCORE_JOINT)
-            capi.analyze(pe, hx, hy_full, np.ones_like(hy_full), host_sets[0][2], hout)
-            res = hout
-        else:
-            res = tb.ensf_analyze(hx, grid, hy_full, r=1.0, seed=7, cycle=1 + q, n_steps=s,
-                                  thinning=stride if stride > 1 else 0,
-                                  precision=args.precision, device=local,
-                                  obs_operator="arctan" if arctan else "linear",
-                                  score_mode=args.score, out=hout)
-        if q >= args.warmup:
-            e2e_times.append(time.perf_counter() - t0)
-    e2e_s = torch.tensor([sum(e2e_times) / len(e2e_times)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-    e2e_value = units_per_gpu * world / float(e2e_s[0])
-    if stride > 1 and k0 != 0:
-        pass  # the e2e leg analyses each rank's shard as its own state (same cost)
+            pe = mkparams(prec, 0, cycle=1 + q)
+            capi.analyze(pe, x_arr, y_arr, np.ones_like(y_arr), hidx, out_arr)
+            return out_arr
+        return tb.ensf_analyze(x_arr, grid, y_arr, r=1.0, seed=7, cycle=1 + q, n_steps=s,
+                               thinning=stride if stride > 1 else 0,
+                               precision=args.precision, device=local,
+                               obs_operator="arctan" if arctan else "linear",
+                               score_mode=args.score, out=out_arr)
+
+    def wall(fn, n_warm, n_timed):
+        for q in range(n_warm):
+            fn(q)
+        if world > 1:
+            dist.barrier()
+        ts = []
+        for q in range(n_timed):
+            t0 = time.perf_counter()
+            fn(n_warm + q)
+            ts.append(time.perf_counter() - t0)
+        t = torch.tensor([sum(ts) / len(ts)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0])
+
+    e2e_s = wall(e2e_call, args.warmup, args.steps)
+    res_bytes = hout.nbytes
+    e2e_value = units_per_gpu * world / e2e_s
     if joint and world > 1:
-        h2d = x0.nbytes + y0.nbytes * (3 if stride > 1 else 2)  # x, y, r (+ idx)
+        h2d = hx.nbytes + hy.nbytes * (3 if stride > 1 else 2)  # x, y, r (+ idx)
     else:
-        h2d = x0.nbytes + y0.nbytes * (2 if stride > 1 else 1) + 8  # x, y (+ idx), one r
-    d2h = res.nbytes + 8
+        # x, y (+ the thinning operator's idx, built from `thinning`), one r
+        h2d = hx.nbytes + hy.nbytes * (2 if stride > 1 else 1) + 8
+    d2h = res_bytes + 8  # the analysis + the divergence word
+
+    # the reference's own call shapes: pageable numpy in, fresh array out
+    # (proj/python/bindings.cpp:140-155) and the C++ Ensemble's member rows
+    # (turbda::analyze, proj/src/ensf.cpp:132 -> turbda_ensf_analyze_rows)
+    variants = {}
+    if not args.no_e2e_variants and world == 1 and not joint:
+        px = np.array(hx)  # pageable copy
+        py_ = np.array(hy)
+        t_page = wall(lambda q: e2e_call(q, out_arr=None, x_arr=px, y_arr=py_), 1, 2)
+        variants["pageable_fresh_out"] = {
+            "value": units_per_gpu / t_page, "unit": UNIT, "s_per_step": t_page,
+            "path": "paper_2407_12168_b200.ensf_analyze(members, grid, y) - the reference "
+                    "binding's signature: pageable float64 numpy in, freshly allocated array out"}
+        rows = [np.array(px[j]) for j in range(m)]  # separately allocated member vectors
+        orows = [np.empty(d) for _ in range(m)]
+        rp = (capi.C.c_void_p * m)(*[r_.ctypes.data for r_ in rows])
+        op = (capi.C.c_void_p * m)(*[o_.ctypes.data for o_ in orows])
+        ridx = None if hidx is None else np.ascontiguousarray(hidx)
+        ones = np.ones(1)
+
+        def rows_call(q):
+            pr = mkparams(prec, capi.R_UNIFORM, cycle=1 + q)
+            capi.analyze_rows(pr, rp, py_, ones, ridx, op)
+
+        t_rows = wall(rows_call, 1, 2)
+        variants["cpp_member_rows"] = {
+            "value": units_per_gpu / t_rows, "unit": UNIT, "s_per_step": t_rows,
+            "path": "turbda_ensf_analyze_rows (what turbda::analyze(const Ensemble&, ...) calls): "
+                    "one pageable std::vector<double> per member in and out"}
+        del px, rows, orows
 
     # --- roofline of the fused analysis kernel -------------------------------
     pk, pk_kind = peaks()
@@ -418,7 +541,7 @@ def main():
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(f"{args.config}_{args.precision}")
+            traffic = json.loads(tf.read_text()).get(f"{args.config}_{args.precision}_{args.score}")
         except ValueError:
             traffic = None
     pair_evals = units_per_launch * m
@@ -437,9 +560,8 @@ def main():
             "achieved": pair_evals / (kern_ms / 1e3), "unit": "pair-evals/s",
             "peak": mufu_peak, "frac": pair_evals / (kern_ms / 1e3) / mufu_peak,
             "peak_source": "16 ex2/clk/SM measured x 148 SMs x sm_max_mhz",
-            "note": "MUFU-only ceiling; for N > 24 (sorted member tiles, up to ~200 members) one "
-                    "pair-eval slot in eight takes its exponential from an FMA-pipe polynomial, "
-                    "so that kernel's own MUFU-bound ceiling is 8/7 of this peak"} if not joint else {
+            "note": "MUFU-only ceiling; a share of the exponentials comes from an FMA-pipe "
+                    "polynomial (DESIGN.md section 3), so the kernel can pass 1.0"} if not joint else {
             "bound": "fp64 pipe (Gram + weighted sum: 2 DFMA per pair-eval)",
             "achieved": 4.0 * pair_evals / (kern_ms / 1e3) / 1e12, "unit": "TFLOP/s",
             "peak": fp64_peak, "frac": 4.0 * pair_evals / (kern_ms / 1e3) / 1e12 / fp64_peak,
@@ -450,28 +572,31 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64" if (joint or prec == capi.FP64) else "f32",
-        "data": "synthetic",
+        "data": "synthetic (N(0,1) forecast members and observations generated on the device)",
         "config": {"workload": desc + (" [joint-norm score extension]" if joint else ""),
                    "score": args.score, "d_per_gpu": d, "d_total": d_total, "members": m,
                    "pseudo_steps": s, "obs_stride": stride,
                    "obs_operator": "arctan" if arctan else "linear",
                    "l2": (f"L2 flushed (512 MB write) before each step, outside its timing; "
-                          f"inputs {set_bytes / 1e6:.0f} MB" if flush else
-                          f"{n_sets} rotating resident input sets ({set_bytes / 1e6:.0f} MB; "
-                          f"{(n_sets - 1) * m * d * 8 / 1e6:.0f} MB > 126 MB L2 pass between "
-                          f"reuses), steps timed back to back"),
+                          f"{n_sets} input sets of {set_bytes / 1e6:.0f} MB" if flush else
+                          f"inputs larger than L2 ({n_sets} set(s) of {set_bytes / 1e6:.0f} MB "
+                          f"forecast > 126 MB L2), steps timed back to back"),
                    "parallelism": f"state-dim shards x{world}"},
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
                 "path": "paper_2407_12168_b200.ensf_analyze(members, grid, y, out=...) "
-                        "with pinned numpy in/out; chunked H2D/compute/D2H pipeline"},
+                        "with pinned numpy in/out; chunked H2D/compute/D2H pipeline",
+                "variants": variants},
         "gpu_launches": int(launches),
         "clocks": clk,
     }
+    if fp64 is not None:
+        line["fp64_value"] = fp64["value"]
+        line["fp64"] = fp64
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        xs, ys, idxs = make_inputs(_cpu_sample(d, m, args.cpu_sample_d), m, stride, 0)
-        cb = reference_rate(xs, ys, idxs, s, 1, 0, arctan=arctan)
+        xs, ys, idxs = make_inputs_host(_cpu_sample(d, m, args.ref_sample_d), m, stride, 0)
+        cb = reference_rate(xs, ys, idxs, s, 3, 1, arctan=arctan)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(line), file=json_out, flush=True)

@@ -85,6 +85,10 @@ typedef enum turbda_precision {
                                      /* the Python binding, bindings/python/      */
                                      /* core.cpp); host or device pointer as the  */
                                      /* other arrays                              */
+#define TURBDA_SHARDED 0x8u          /* turbda_diag: `members` / `truth` are this */
+                                     /* rank's shard of a state split over the    */
+                                     /* ranks of turbda_comm_init; the partial    */
+                                     /* sums are allreduced over them             */
 
 typedef struct turbda_status {
     int32_t code;              /* turbda_code                                   */
@@ -187,7 +191,11 @@ TURBDA_API int turbda_score(const double* z, int64_t d, double t, const double* 
 
 /* out[0] = sum_k (mean_k - truth_k)^2 (0 when truth == NULL),
  * out[1] = sum_{j,k} (x_jk - mean_k)^2.  members / truth are host or device
- * buffers per flags; out is always a host double[2]. */
+ * buffers per flags; out is always a host double[2].  The sums are taken in
+ * a fixed order (fixed grid, two-stage reduction): bitwise reproducible.
+ * With TURBDA_SHARDED (and a communicator on `device`) they are summed over
+ * the communicator's ranks; without it the call is local even when a
+ * communicator exists. */
 TURBDA_API int turbda_diag(const double* members, int32_t n_members, int64_t d, const double* truth,
                 double* out, int32_t device, uint32_t flags, void* stream,
                 turbda_status* status);
@@ -197,8 +205,10 @@ TURBDA_API int turbda_diag(const double* members, int32_t n_members, int64_t d, 
  * per GPU).  The joint score mode exchanges the per-step distances through
  * it; the componentwise mode needs none, but with a communicator a window
  * (d_local < d_total) min-reduces its divergence verdict, so every rank
- * reports the unsharded run's SamplerDivergedError, and turbda_diag sums
- * its partials over the ranks.  NCCL is loaded on first use
+ * reports the unsharded run's SamplerDivergedError, and turbda_diag with
+ * TURBDA_SHARDED sums its partials over the ranks.  A rank whose window is
+ * empty (d_local == 0) still joins every collective of the call, so its
+ * peers never wait on it.  NCCL is loaded on first use
  * (dlopen("libnccl.so.2"), the copy torch already loaded when present).
  *   rank 0: turbda_comm_unique_id(id) -> broadcast the 128 bytes -> every
  *   rank: turbda_comm_init(device, rank, world, id).

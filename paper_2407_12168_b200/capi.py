@@ -23,6 +23,7 @@ FP32, FP64 = 0, 1
 INPUTS_ON_DEVICE = 0x1
 ASYNC = 0x2
 R_UNIFORM = 0x4
+SHARDED = 0x8
 
 
 class EnsfParams(C.Structure):
@@ -205,6 +206,18 @@ def analyze(p: EnsfParams, forecast, y, r_diag, obs_idx, out, stream: int | None
     return st
 
 
+def analyze_rows(p: EnsfParams, forecast_rows, y, r_diag, obs_idx, analysis_rows):
+    """Raw C-ABI call with one host pointer per member row in and out (the
+    reference ``Ensemble::members`` layout): ``forecast_rows`` /
+    ``analysis_rows`` are ctypes ``c_void_p`` arrays of length n_members."""
+    st = Status()
+    code = lib().turbda_ensf_analyze_rows(C.byref(p), C.cast(forecast_rows, C.c_void_p), _ptr(y),
+                                          _ptr(r_diag), _ptr(obs_idx),
+                                          C.cast(analysis_rows, C.c_void_p), C.byref(st))
+    _check(code, st)
+    return st
+
+
 def check(device: int, p: EnsfParams) -> Status:
     st = Status()
     _check(lib().turbda_ensf_check(device, C.byref(p), C.byref(st)), st)
@@ -362,13 +375,16 @@ def relax_spread(analysis, forecast, factor, device=-1):
     return out
 
 
-def diag(members, truth=None, device=-1):
+def diag(members, truth=None, device=-1, sharded=False):
+    """(sum (mean - truth)^2, sum dev^2) in a fixed order; ``sharded``: the
+    arrays are this rank's shard and the sums are allreduced over the
+    device's communicator (TURBDA_SHARDED)."""
     x = np.ascontiguousarray(members, np.float64)
     t = None if truth is None else np.ascontiguousarray(truth, np.float64)
     out = (C.c_double * 2)()
     st = Status()
-    _check(lib().turbda_diag(_ptr(x), x.shape[0], x.shape[1], _ptr(t), out, device, 0, None,
-                             C.byref(st)), st)
+    _check(lib().turbda_diag(_ptr(x), x.shape[0], x.shape[1], _ptr(t), out, device,
+                             SHARDED if sharded else 0, None, C.byref(st)), st)
     return float(out[0]), float(out[1])
 
 

@@ -88,6 +88,7 @@ struct Workspace {
     int device = -1;
     cudaStream_t stream = nullptr;
     DevBuf x, z, xt, ab, steps, batches, status, out, y, r, idx;
+    DevBuf obs_tmp, diag;                       // obs sort scratch, diag partials
     unsigned long long* status_host = nullptr;  // pinned
     void* comm = nullptr;                       // ncclComm_t (joint mode, sharded)
     int comm_world = 1;
@@ -238,6 +239,29 @@ int validate_host_obs(const turbda_ensf_params* p, const double* r, const int64_
         for (int64_t q = 0; q < p->obs_dim; ++q)
             if (idx[q] < 0 || idx[q] >= p->d_total)
                 return fail(st, TURBDA_DIMENSION, "observation: index outside the state");
+    return TURBDA_OK;
+}
+
+// Selection indices in strictly increasing order (every stride operator):
+// the observation prep writes them directly instead of sorting.
+bool strictly_increasing(const int64_t* idx, int64_t n) {
+    for (int64_t q = 1; q < n; ++q)
+        if (idx[q] <= idx[q - 1]) return false;
+    return true;
+}
+
+// {A, B} of a selection operator for the window [k0, k0 + dl) into ab.
+int select_prep(Workspace* w, const double* dy, const double* dr, const int64_t* didx,
+                const int64_t* host_idx, int64_t obs_dim, int obs_kind, int64_t k0, int64_t dl,
+                double2* ab, int64_t r_stride, cudaStream_t s, turbda_status* st) {
+    const bool inc = host_idx && strictly_increasing(host_idx, obs_dim);
+    size_t bytes = 0;
+    if (!inc) {
+        bytes = obs_prep_scratch_bytes(obs_dim);
+        TB_CUDA(w->obs_tmp.reserve(std::max<size_t>(bytes, 1)));
+    }
+    TB_CUDA(launch_obs_prep(dy, dr, didx, obs_dim, obs_kind, k0, dl, ab, s, r_stride, inc,
+                            w->obs_tmp.p, bytes));
     return TURBDA_OK;
 }
 
@@ -443,8 +467,12 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
                                         cudaMemcpyHostToDevice, s));
             }
         }
-        TB_CUDA(cudaEventRecord(w->ev_ready, s));
     }
+    if (!obs_dense(p->obs_kind))
+        if (int rc = select_prep(w, dy, dr, didx, on_dev ? nullptr : idx, p->obs_dim, p->obs_kind,
+                                 p->k0 + win.k0_local, dl, w->ab.as<double2>(), r_stride, s, st))
+            return rc;
+    if (!on_dev) TB_CUDA(cudaEventRecord(w->ev_ready, s));
 
     KernelArgs a{};
     a.d_total = p->d_total;
@@ -499,12 +527,9 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
         }
         const int64_t k0c = p->k0 + col;
         double2* abc = w->ab.as<double2>() + c.k0_local;
-        const bool dense = obs_dense(p->obs_kind);
-        const double* yc = dense ? dy + c.k0_local : dy;
-        const double* rc_ = (dense && !r_uni) ? dr + c.k0_local : dr;
-        const int64_t nobs = dense ? c.dl : p->obs_dim;
-        TB_CUDA(launch_obs_prep(yc, rc_, didx, nobs, p->obs_kind, k0c, c.dl, abc, cs, r_stride));
-        ++g_launches;
+        if (obs_dense(p->obs_kind))
+            TB_CUDA(launch_obs_prep(dy + c.k0_local, r_uni ? dr : dr + c.k0_local, nullptr, c.dl,
+                                    p->obs_kind, k0c, c.dl, abc, cs, r_stride, true, nullptr, 0));
         a.k0 = k0c;
         a.dl = c.dl;
         if (prof.a) TB_CUDA(cudaEventRecord(prof.a, cs));
@@ -718,8 +743,12 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
     TB_CUDA(cudaMemsetAsync(dstatus, 0xff, sizeof(unsigned long long), s));
 
     const int64_t k0g = p->k0 + win.k0_local;
-    TB_CUDA(launch_obs_prep(dy, dr, didx, dense ? dl : p->obs_dim, p->obs_kind, k0g, dl,
-                            w->ab.as<double2>(), s, r_uni ? 0 : 1));
+    if (dense)
+        TB_CUDA(launch_obs_prep(dy, dr, nullptr, dl, p->obs_kind, k0g, dl, w->ab.as<double2>(), s,
+                                r_uni ? 0 : 1, true, nullptr, 0));
+    else if (int rc = select_prep(w, dy, dr, didx, on_dev ? nullptr : idx, p->obs_dim, p->obs_kind,
+                                  k0g, dl, w->ab.as<double2>(), r_uni ? 0 : 1, s, st))
+        return rc;
     KernelArgs a{};
     a.d_total = p->d_total;
     a.k0 = k0g;
@@ -762,7 +791,7 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
         g_prof_pending.push_back(prof);
     }
     TB_CUDA(launch_relax_f64(z, dx, m, dl, p->relax_factor, dout, s));
-    g_launches += 3 + 4 * uint64_t(p->n_steps);
+    g_launches += 2 + 4 * uint64_t(p->n_steps);
     if (int rc = reduce_verdict_across_ranks(p, w, dstatus, s, st)) return rc;
     if (on_dev && (p->flags & TURBDA_ASYNC)) {
         TB_CUDA(ws_release(w, s, true));
@@ -781,6 +810,49 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
                                       size_t(m), cudaMemcpyDeviceToHost, s));
         }
     }
+    TB_CUDA(cudaStreamSynchronize(s));
+    TB_CUDA(ws_release(w, s, false));
+    return diverged(p, *w->status_host, st);
+}
+
+// An empty window (d_local == 0) of a state sharded over a communicator:
+// nothing to analyse, but the peers' collectives must still complete, so the
+// rank joins each of them with a neutral contribution - in joint mode one
+// zero [G | nz | nx] buffer per pseudo-step, then the divergence verdict
+// (kNoDivergence) - and reports the reduced verdict like its peers.
+int join_empty_window(const turbda_ensf_params* p, int device, cudaStream_t user_stream,
+                      turbda_status* st) {
+    TB_CUDA(cudaSetDevice(device));
+    Workspace* w = workspace(device);
+    std::lock_guard<std::mutex> lk(w->mu);
+    if (!w->comm || w->comm_world <= 1 || p->d_total == 0) return TURBDA_OK;
+    if (int rc = ws_init(w, st)) return rc;
+    const bool on_dev = (p->flags & TURBDA_INPUTS_ON_DEVICE) != 0;
+    cudaStream_t s = user_stream ? user_stream : (on_dev ? cudaStreamLegacy : w->stream);
+    TB_CUDA(ws_acquire(w, s));
+    NcclApi* api = nccl_api();
+    if (!api) return fail(st, TURBDA_CUDA, "libnccl.so.2 not loadable");
+    const ncclComm_t comm = static_cast<ncclComm_t>(w->comm);
+    if (p->score_mode == TURBDA_SCORE_JOINT) {
+        const JointPlan pl = joint_plan(p->n_members, p->n_members, 1);
+        TB_CUDA(w->jred.reserve(sizeof(double) * pl.red_len));
+        for (int step = 0; step < p->n_steps; ++step) {
+            TB_CUDA(cudaMemsetAsync(w->jred.p, 0, sizeof(double) * pl.red_len, s));
+            const ncclResult_t r = api->all_reduce(w->jred.p, w->jred.p, pl.red_len, ncclDouble,
+                                                   ncclSum, comm, s);
+            if (r != ncclSuccess) return nccl_fail(st, api, r, "ncclAllReduce");
+        }
+    }
+    TB_CUDA(w->status.reserve(64));
+    unsigned long long* dstatus = w->status.as<unsigned long long>();
+    TB_CUDA(cudaMemsetAsync(dstatus, 0xff, sizeof(unsigned long long), s));
+    if (int rc = reduce_verdict_across_ranks(p, w, dstatus, s, st)) return rc;
+    if (on_dev && (p->flags & TURBDA_ASYNC)) {
+        TB_CUDA(ws_release(w, s, true));
+        return TURBDA_OK;
+    }
+    TB_CUDA(cudaMemcpyAsync(w->status_host, dstatus, sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s));
     TB_CUDA(cudaStreamSynchronize(s));
     TB_CUDA(ws_release(w, s, false));
     return diverged(p, *w->status_host, st);
@@ -845,7 +917,9 @@ int analyze_impl(const turbda_ensf_params* p, const double* forecast, const doub
     if (dev0 + ndev > avail) return fail(st, TURBDA_CUDA, "device_count exceeds visible devices");
     if (on_dev && ndev > 1)
         return fail(st, TURBDA_CONFIG, "device_count > 1 needs host buffers");
-    if (p->d_local == 0) return TURBDA_OK;
+    if (p->d_local == 0)
+        return ndev == 1 ? join_empty_window(p, dev0, static_cast<cudaStream_t>(stream), st)
+                         : TURBDA_OK;
 
     const bool joint = p->score_mode == TURBDA_SCORE_JOINT;
     if (ndev == 1) {
@@ -1045,9 +1119,12 @@ int turbda_score(const double* z, int64_t d, double t, const double* forecast, i
                 TB_CUDA(cudaMemcpyAsync(w->idx.p, obs_idx, sizeof(int64_t) * size_t(obs_dim),
                                         cudaMemcpyHostToDevice, s));
         }
-        TB_CUDA(launch_obs_prep(w->y.as<double>(), w->r.as<double>(), w->idx.as<int64_t>(), obs_dim,
-                                obs_kind, 0, d, w->ab.as<double2>(), s));
-        ++g_launches;
+        if (obs_dense(obs_kind))
+            TB_CUDA(launch_obs_prep(w->y.as<double>(), w->r.as<double>(), nullptr, d, obs_kind, 0, d,
+                                    w->ab.as<double2>(), s, 1, true, nullptr, 0));
+        else if (int rc = select_prep(w, w->y.as<double>(), w->r.as<double>(), w->idx.as<int64_t>(),
+                                      obs_idx, obs_dim, obs_kind, 0, d, w->ab.as<double2>(), 1, s, st))
+            return rc;
         dab = w->ab.as<double2>();
         damp = damping_t - t;
     }
@@ -1074,8 +1151,8 @@ int turbda_diag(const double* members, int32_t m, int64_t d, const double* truth
     if (int rc = ws_init(w, st)) return rc;
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : w->stream;
     TB_CUDA(ws_acquire(w, s));
-    TB_CUDA(w->status.reserve(64));
-    double* dsum = reinterpret_cast<double*>(w->status.as<unsigned char>() + 16);
+    TB_CUDA(w->diag.reserve(sizeof(double) * diag_scratch_doubles()));
+    double* dsum = w->diag.as<double>();
     const size_t md = size_t(m) * size_t(d);
     const double* dx = members;
     const double* dt = truth;
@@ -1090,9 +1167,10 @@ int turbda_diag(const double* members, int32_t m, int64_t d, const double* truth
         }
     }
     TB_CUDA(launch_diag(dx, m, d, dt, dsum, s));
-    ++g_launches;
-    if (w->comm && w->comm_world > 1) {
-        // a state sharded over the communicator's ranks: global partial sums
+    if (flags & TURBDA_SHARDED) {
+        // this rank's shard of a state split over the communicator's ranks
+        if (!w->comm || w->comm_world <= 1)
+            return fail(st, TURBDA_CONFIG, "TURBDA_SHARDED needs turbda_comm_init on this device");
         NcclApi* api = nccl_api();
         if (!api) return fail(st, TURBDA_CUDA, "libnccl.so.2 not loadable");
         const ncclResult_t r = api->all_reduce(dsum, dsum, 2, ncclDouble, ncclSum,

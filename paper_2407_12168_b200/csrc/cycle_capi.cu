@@ -20,6 +20,7 @@
 #include "ensf_device.h"
 #include "host_rng.h"
 #include "philox.cuh"
+#include "reduce.cuh"
 #include "sqg_gpu.h"
 #include "turbda_b200.h"
 
@@ -173,12 +174,16 @@ __global__ void model_error_kernel(double* __restrict__ x, int m, int64_t d,
     }
 }
 
-__global__ void sum_squares_kernel(const double* __restrict__ x, size_t n, double* __restrict__ out) {
+// sum of squares of the climatology (model-error base amplitude,
+// proj/src/forecast.cpp:77-100) in a fixed order: one partial per CTA of a
+// fixed grid, summed in CTA order (reduce.cuh)
+constexpr int kSumSqBlocks = 592;
+__global__ void __launch_bounds__(256) sum_squares_kernel(const double* __restrict__ x, size_t n,
+                                                          double* __restrict__ part) {
     double s = 0.0;
     for (size_t q = size_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n; q += size_t(gridDim.x) * blockDim.x)
         s += x[q] * x[q];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+    block_sum2_to(s, 0.0, part + 2 * blockIdx.x);
 }
 
 struct DeviceBuffer {
@@ -526,9 +531,10 @@ int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* re
     double base = e->me_base_amplitude;
     if (!(base > 0.0)) {
         DeviceBuffer acc;
-        CY_CUDA(cudaMalloc(&acc.p, sizeof(double)));
-        CY_CUDA(cudaMemsetAsync(acc.p, 0, sizeof(double), s));
-        sum_squares_kernel<<<592, 256, 0, s>>>(clim, size_t(n_clim) * size_t(d), acc.as<double>());
+        CY_CUDA(cudaMalloc(&acc.p, sizeof(double) * (2 + 2 * kSumSqBlocks)));
+        sum_squares_kernel<<<kSumSqBlocks, 256, 0, s>>>(clim, size_t(n_clim) * size_t(d),
+                                                        acc.as<double>() + 2);
+        sum_partials_kernel<<<1, 32, 0, s>>>(acc.as<double>() + 2, kSumSqBlocks, acc.as<double>());
         double ss = 0.0;
         CY_CUDA(cudaMemcpyAsync(&ss, acc.p, sizeof ss, cudaMemcpyDeviceToHost, s));
         CY_CUDA(cudaStreamSynchronize(s));
@@ -581,7 +587,7 @@ int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* re
     CY_CUDA(cudaMalloc(&dfrac.p, sizeof(double) * 8));
     CY_CUDA(cudaMemcpyAsync(dprob.p, e->me_prob, sizeof(double) * 8, cudaMemcpyHostToDevice, s));
     CY_CUDA(cudaMemcpyAsync(dfrac.p, e->me_frac, sizeof(double) * 8, cudaMemcpyHostToDevice, s));
-    CY_CUDA(cudaMalloc(&ddiag.p, sizeof(double) * 2));
+    CY_CUDA(cudaMalloc(&ddiag.p, sizeof(double) * diag_scratch_doubles()));
 
     SqgGpu model;
     {

@@ -52,10 +52,15 @@ inline bool obs_arctan(int kind) { return kind == 2 || kind == 3; }
 // Divergence word: min over ((particle << 32) | step); ~0 = none.
 constexpr unsigned long long kNoDivergence = ~0ull;
 
-// obs (y, r, idx) -> per-coordinate {A = sum 1/r, B = sum y/r} over the window
+// obs (y, r, idx) -> per-coordinate {A = sum 1/r, B = sum y/r} over the
+// window, summed in observation order without atomics.  Selection operators
+// with strictly increasing indices (idx_increasing) write directly; any other
+// index order is stably sorted first, in `scratch` (obs_prep_scratch_bytes).
+size_t obs_prep_scratch_bytes(int64_t obs_dim);
 cudaError_t launch_obs_prep(const double* y, const double* r, const int64_t* idx,
                             int64_t obs_dim, int obs_kind, int64_t k0, int64_t dl,
-                            double2* ab, cudaStream_t st, int64_t r_stride = 1);
+                            double2* ab, cudaStream_t st, int64_t r_stride,
+                            bool idx_increasing, void* scratch, size_t scratch_bytes);
 
 // full fused analysis into z (fp32 or fp64 scratch, [m][dl]).  The fp32 path
 // first converts (and, without minibatches, sorts per coordinate) the
@@ -105,7 +110,10 @@ cudaError_t launch_joint_update(const KernelArgs& a, const double* x, const doub
                                 double* z, unsigned long long* status, bool f32_noise,
                                 cudaStream_t st);
 
-// rmse / spread partial sums: out[0] = sum (mean - truth)^2, out[1] = sum dev^2
+// rmse / spread sums in a fixed order: out[0] = sum (mean - truth)^2,
+// out[1] = sum dev^2; `out` holds diag_scratch_doubles() doubles (the
+// per-CTA partials follow the two results)
+size_t diag_scratch_doubles();
 cudaError_t launch_diag(const double* x, int m, int64_t d, const double* truth, double* out,
                         cudaStream_t st);
 

@@ -25,6 +25,9 @@
 #include "ensf_device.h"
 #include "bulk_copy.cuh"
 #include "philox.cuh"
+#include "reduce.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
 
 namespace tb200 {
 
@@ -39,6 +42,19 @@ __device__ __forceinline__ float ex2f(float x) {
 }
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// one pseudo-step's coefficients: a warp-uniform 32 B read (L1 broadcast)
+__device__ __forceinline__ StepF32 load_step(const StepF32* p) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    return StepF32{a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+}
 
 // proj/include/turbda/fastexp.hpp:13-50, restated for the device.
 __device__ __forceinline__ double fast_exp_nonpos_dev(double x) {
@@ -165,12 +181,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
     static_assert(!(kGlobalX && kSorted), "very large ensembles use the two-pass member loop");
     constexpr int U = 4;  // member-loop unroll
     extern __shared__ float4 smem[];
-    StepF32* cs = reinterpret_cast<StepF32*>(smem);
     // the tile's members: shared memory, or (ensembles too large for it)
     // read straight from the fp32 tile in global memory through L1/L2
     const float2* xs = kGlobalX ? reinterpret_cast<const float2*>(
                                       xt + size_t(blockIdx.x) * size_t(a.m) * kTile)
-                                : reinterpret_cast<const float2*>(cs + a.n_steps);
+                                : reinterpret_cast<const float2*>(smem);
     const float* xsf = reinterpret_cast<const float*>(xs);
 
     const int lane = threadIdx.x & 31;
@@ -180,20 +195,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
     const int64_t kl = tile0 + 2 * lane;  // local coordinate of this lane's pair
     const bool aligned = ((a.dl & 1) == 0);
 
-    // the step table and the tile's members (fp32 [m][64], sorted per column
-    // when kSorted, contiguous by prep_tiles_kernel) arrive by two TMA bulk
-    // copies issued by one thread while the others set up their pairs
+    // the tile's members (fp32 [m][64], sorted per column when kSorted,
+    // contiguous by prep_tiles_kernel) arrive by one TMA bulk copy issued by
+    // one thread while the others set up their pairs.  The per-step
+    // coefficients are read from global memory (warp-uniform, L1-resident),
+    // so any n_steps fits.
     __shared__ uint64_t tile_bar;
-    if (threadIdx.x == 0) mbar_init(&tile_bar, 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const uint32_t step_bytes = uint32_t(sizeof(StepF32)) * uint32_t(a.n_steps);
-        const uint32_t tile_bytes = kGlobalX ? 0u : uint32_t(sizeof(float)) * uint32_t(a.m) * kTile;
-        mbar_arrive_expect_tx(&tile_bar, step_bytes + tile_bytes);
-        bulk_copy_g2s(cs, steps, step_bytes, &tile_bar);
-        if (!kGlobalX)
-            bulk_copy_g2s(cs + a.n_steps, xt + size_t(blockIdx.x) * size_t(a.m) * kTile,
-                          tile_bytes, &tile_bar);
+    if (!kGlobalX) {
+        if (threadIdx.x == 0) mbar_init(&tile_bar, 1);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t tile_bytes = uint32_t(sizeof(float)) * uint32_t(a.m) * kTile;
+            mbar_arrive_expect_tx(&tile_bar, tile_bytes);
+            bulk_copy_g2s(smem, xt + size_t(blockIdx.x) * size_t(a.m) * kTile, tile_bytes,
+                          &tile_bar);
+        }
     }
     // likelihood operator for this pair: B - A z with A = sum 1/r, B = sum y/r
     float2 A2 = f2(0.f), B2 = f2(0.f);
@@ -213,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
     // probes top, top/2, .., 1 reach pos <= 2 top - 1 >= J - 1; pos = J - 1
     // when all J members have u > 0 still yields the right pair (J-2, J-1)
     while (top * 2 < a.j_batch) top *= 2;
-    mbar_wait(&tile_bar, 0);  // step table and member tile have landed
+    if (!kGlobalX) mbar_wait(&tile_bar, 0);  // the member tile has landed
 
     const int i0 = (blockIdx.y * nwarps + warp) * P;
     const uint64_t kg = uint64_t(a.k0 + kl);  // global coordinate of the pair's first entry
@@ -227,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
     }
 
     for (int s = 0; s < a.n_steps; ++s) {
-        const StepF32 c = cs[s];
+        const StepF32 c = load_step(steps + s);
         const float2 nas2 = f2(c.nas);
         const int32_t* bt = kMinibatch ? batches + size_t(s) * size_t(a.j_batch) : nullptr;
 
@@ -337,8 +353,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
         const uint64_t n0 = uint64_t(s + 1) * uint64_t(a.d_total) + kg;
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            const float2 q = make_float2(__fdividef(num[p].x, den[p].x),
-                                         __fdividef(num[p].y, den[p].y));
+            // one MUFU.RCP for the pair: 1 / (den.x den.y).  Both sums lie in
+            // [2^-60, J] (the redo guarantees the lower bound), so the product
+            // is a normal float; a non-finite one only marks a diverged pair.
+            const float rr = rcp_approx(den[p].x * den[p].y);
+            const float2 q = __fmul2_rn(__fmul2_rn(num[p], make_float2(den[p].y, den[p].x)),
+                                        f2(rr));
             float2 lik;
             if (a.obs_atan) {
                 // h(z) = atan(z): H'^T R^-1 (y - h) = (B - A atan z) / (1 + z^2)
@@ -424,8 +444,7 @@ __global__ void __launch_bounds__(128) ensf_f64_kernel(KernelArgs a, const doubl
                                                        double* __restrict__ z_out,
                                                        unsigned long long* __restrict__ status) {
     extern __shared__ double2 smem2[];
-    StepF64* cs = reinterpret_cast<StepF64*>(smem2);
-    double2* xs = reinterpret_cast<double2*>(cs + a.n_steps);  // [m][32] when kSmemX
+    double2* xs = smem2;  // [m][32] when kSmemX; steps are read from global
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -434,7 +453,6 @@ __global__ void __launch_bounds__(128) ensf_f64_kernel(KernelArgs a, const doubl
     const int64_t kl = tile0 + 2 * lane;
     const bool aligned = ((a.dl & 1) == 0);
 
-    for (int q = threadIdx.x; q < a.n_steps; q += blockDim.x) cs[q] = steps[q];
     if (kSmemX) {
         for (int q = threadIdx.x; q < a.m * 32; q += blockDim.x) {
             const int j = q >> 5, l = q & 31;
@@ -468,7 +486,7 @@ __global__ void __launch_bounds__(128) ensf_f64_kernel(KernelArgs a, const doubl
     }
 
     for (int s = 0; s < a.n_steps; ++s) {
-        const StepF64 c = cs[s];
+        const StepF64 c = steps[s];
         const int32_t* bt = kMinibatch ? batches + size_t(s) * size_t(a.j_batch) : nullptr;
         double mx[P], my[P];
 #pragma unroll
@@ -580,8 +598,6 @@ __global__ void relax_kernel(const T* __restrict__ z, const double* __restrict__
 }
 
 // obs -> per-coordinate {A, B}.  Identity: one entry per coordinate.
-// Selection: entries whose global index falls in the window are scattered
-// (duplicate indices add, as adjoint_scatter does, proj/src/observation.cpp:18-27).
 // r_stride 0: one error variance for every observation (TURBDA_R_UNIFORM)
 __global__ void obs_identity_kernel(const double* __restrict__ y, const double* __restrict__ r,
                                     int64_t r_stride, int64_t dl, double2* __restrict__ ab) {
@@ -592,17 +608,48 @@ __global__ void obs_identity_kernel(const double* __restrict__ y, const double* 
     }
 }
 
-__global__ void obs_select_kernel(const double* __restrict__ y, const double* __restrict__ r,
-                                  int64_t r_stride, const int64_t* __restrict__ idx,
-                                  int64_t obs_dim, int64_t k0, int64_t dl,
-                                  double2* __restrict__ ab) {
+// Selection, strictly increasing indices (every stride operator,
+// make_grid_operator, proj/src/observation.cpp:29-41): at most one entry per
+// coordinate, written directly.
+__global__ void obs_select_unique_kernel(const double* __restrict__ y, const double* __restrict__ r,
+                                         int64_t r_stride, const int64_t* __restrict__ idx,
+                                         int64_t obs_dim, int64_t k0, int64_t dl,
+                                         double2* __restrict__ ab) {
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= obs_dim) return;
     const int64_t k = idx[q] - k0;
     if (k < 0 || k >= dl) return;
     const double inv = 1.0 / r[q * r_stride];
-    atomicAdd(&ab[k].x, inv);
-    atomicAdd(&ab[k].y, y[q] * inv);
+    ab[k] = make_double2(inv, y[q] * inv);
+}
+
+__global__ void iota_kernel(int32_t* __restrict__ v, int64_t n) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q < n) v[q] = int32_t(q);
+}
+
+// Selection, any index order (duplicates add, as adjoint_scatter does,
+// proj/src/observation.cpp:18-27): (index, position) pairs stably sorted by
+// index; the head of every run of equal indices sums its run in observation
+// order.  No atomics: the sums are bitwise reproducible.
+__global__ void obs_select_runs_kernel(const double* __restrict__ y, const double* __restrict__ r,
+                                       int64_t r_stride, const int64_t* __restrict__ keys,
+                                       const int32_t* __restrict__ pos, int64_t obs_dim, int64_t k0,
+                                       int64_t dl, double2* __restrict__ ab) {
+    const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= obs_dim) return;
+    const int64_t key = keys[t];
+    if (t > 0 && keys[t - 1] == key) return;
+    const int64_t k = key - k0;
+    if (k < 0 || k >= dl) return;
+    double A = 0.0, B = 0.0;
+    for (int64_t u = t; u < obs_dim && keys[u] == key; ++u) {
+        const int64_t q = pos[u];
+        const double inv = 1.0 / r[q * r_stride];
+        A += inv;
+        B += y[q] * inv;
+    }
+    ab[k] = make_double2(A, B);
 }
 
 // single-vector componentwise score, proj/src/ensf.cpp:33-64,96-106
@@ -637,9 +684,17 @@ __global__ void score_kernel(const double* __restrict__ z, const double* __restr
     out[k] = s;
 }
 
-// rmse/spread partial sums (proj/src/ensemble.cpp:18-43)
-__global__ void diag_kernel(const double* __restrict__ x, int m, int64_t d,
-                            const double* __restrict__ truth, double* __restrict__ out) {
+// rmse/spread partial sums (proj/src/ensemble.cpp:18-43) in a fixed order:
+// a fixed grid of kDiagBlocks CTAs, each thread strides the coordinates in a
+// fixed sequence, the warp and block combine in a fixed tree, and one warp
+// sums the block partials in block order.  No atomics: bitwise reproducible
+// from run to run (the reference's byte-identical metrics contract,
+// proj/tests/test_osse.cpp:163-179).
+constexpr int kDiagBlocks = 592;  // 4 x 148 SMs
+
+__global__ void __launch_bounds__(256) diag_kernel(const double* __restrict__ x, int m, int64_t d,
+                                                   const double* __restrict__ truth,
+                                                   double* __restrict__ part) {
     double e2 = 0.0, v2 = 0.0;
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < d;
          k += int64_t(gridDim.x) * blockDim.x) {
@@ -655,99 +710,32 @@ __global__ void diag_kernel(const double* __restrict__ x, int m, int64_t d,
             v2 += dv * dv;
         }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-        e2 += __shfl_xor_sync(0xffffffffu, e2, o);
-        v2 += __shfl_xor_sync(0xffffffffu, v2, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicAdd(out, e2);
-        atomicAdd(out + 1, v2);
-    }
+    block_sum2_to(e2, v2, part + 2 * blockIdx.x);
 }
 
 int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
 
 // Ensembles whose fp32 tile ([m][64] floats) does not fit next to the step
 // table in shared memory read their members from global memory (L1/L2).
-bool f32_members_global(int m, int n_steps) {
-    return sizeof(StepF32) * size_t(n_steps) + sizeof(float) * 64 * size_t(m) > 200 * 1024;
+bool f32_members_global(int m) { return sizeof(float) * 64 * size_t(m) > 200 * 1024; }
+
+// Tuning knobs read once per process (experiments and the exact-shift
+// cross-check in tests/; the defaults are the measured best):
+//   TURBDA_F32_POLY=k         share of the exponentials taken by the FMA-pipe
+//                             polynomial: one (member, particle) slot in k of
+//                             the 16-slot unrolled member loop; 0 = all MUFU
+//   TURBDA_F32_EXACT_SHIFT=1  always take the reference's exact softmax
+//                             shift first (no shift-free pass)
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
 }
 
-// fp32 kernel variant for experiments (TURBDA_F32_VARIANT): 0 default,
-// 1 MUFU/FMA-polynomial exp split, 2 never sort, 3 always sort.
-int f32_variant() {
-    static const int v = [] {
-        const char* e = std::getenv("TURBDA_F32_VARIANT");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
-template <int P>
-cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab,
-                         const StepF32* steps, const int32_t* batches, float* z,
-                         unsigned long long* status, cudaStream_t st, bool sorted) {
-    // warps per CTA: enough to cover the members, at most 8
-    const int groups = (a.m + P - 1) / P;
-    static const int ctas_env = [] {
-        const char* e = std::getenv("TURBDA_F32_CTAS");
-        return e ? std::atoi(e) : 0;
-    }();
-    const int ctas = ctas_env ? ctas_env : (sorted ? 3 : 4);
-    const bool global_x = f32_members_global(a.m, a.n_steps);
-    const size_t smem = sizeof(StepF32) * size_t(a.n_steps) +
-                        (global_x ? 0 : sizeof(float2) * 32 * size_t(a.m));
-    // variants 13-17: wide CTAs (16 / 32 warps) for tiles whose shared memory
-    // allows only one CTA per SM (config 4); the default picks kWideDefault there
-    constexpr int kWideDefault = 16;
-    const bool one_cta_per_sm = !global_x && smem * 2 > size_t(227) * 1024;
-    const int variant = (sorted && f32_variant() == 0 && ctas_env == 0 && one_cta_per_sm)
-                            ? kWideDefault : f32_variant();
-    const int wmax = (sorted && ctas == 7) ? 4
-                     : (sorted && (variant == 13 || variant == 15)) ? 16
-                     : (sorted && (variant == 14 || variant == 16)) ? 32
-                     : (sorted && variant == 17) ? 16 : 8;
-    const int nw = groups < wmax ? groups : wmax;
-    const dim3 block(32 * nw);
-    const dim3 grid(unsigned((a.dl + kTile - 1) / kTile), unsigned((groups + nw - 1) / nw));
-    // letting ptxas take more registers (1 CTA/SM) loses ~20%.
-    // Sorted tiles (N > 24): 4 CTAs of 256 threads per SM (64 registers) with
-    // one in eight exponentials on the FMA-pipe polynomial when four member
-    // tiles fit in shared memory (config 2 13.18 -> 12.47 ms, config 5
-    // 809 -> 752 ms; tools/variant_sweep.sh).  When shared memory allows only
-    // one CTA per SM (config 4, N = 512: a 128 KB member tile) that CTA is
-    // 32 warps (64 registers) with the same one-in-eight polynomial share:
-    // config 4 6675 -> 5607 ms (8 warps all-MUFU 6675, 16 warps 6199,
-    // 32 warps 6169, 16 warps + 1/8 poly 5727, 16 warps + 1/4 poly 5990).
-    // Otherwise 3 CTAs all-MUFU.  Brute-force shift (N <= 24): 4 CTAs, all-MUFU (config 3; the
-    // polynomial is neutral there).  TURBDA_F32_CTAS / TURBDA_F32_VARIANT
-    // override for experiments.
-    const bool sorted_fast = sorted && variant == 0 && ctas_env == 0 &&
-                             smem * 4 <= size_t(227) * 1024;
-    auto kern = global_x ? (a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3, true>
-                                        : ensf_f32_kernel<P, false, false, 0, 3, true>)
-                : a.minibatch ? ensf_f32_kernel<P, true, false, 0, 3>
-                : !sorted   ? (variant == 6 ? ensf_f32_kernel<P, false, false, 0, 4, false, 256, false>
-                               : variant == 10 ? ensf_f32_kernel<P, false, false, 8, 4>
-                               : variant == 11 ? ensf_f32_kernel<P, false, false, 16, 4>
-                               : variant == 12 ? ensf_f32_kernel<P, false, false, 4, 4>
-                               : ctas == 4  ? ensf_f32_kernel<P, false, false, 0, 4>
-                                            : ensf_f32_kernel<P, false, false, 0, 3>)
-                : sorted_fast  ? ensf_f32_kernel<P, false, true, 8, 4>
-                : variant == 1 ? ensf_f32_kernel<P, false, true, 8, 3>
-                : variant == 13 ? ensf_f32_kernel<P, false, true, 0, 1, false, 512>
-                : variant == 14 ? ensf_f32_kernel<P, false, true, 0, 1, false, 1024>
-                : variant == 15 ? ensf_f32_kernel<P, false, true, 8, 1, false, 512>
-                : variant == 16 ? ensf_f32_kernel<P, false, true, 8, 1, false, 1024>
-                : variant == 17 ? ensf_f32_kernel<P, false, true, 4, 1, false, 512>
-                : variant == 7 ? ensf_f32_kernel<P, false, true, 16, 3>
-                : variant == 8 ? ensf_f32_kernel<P, false, true, 4, 3>
-                : variant == 9 ? ensf_f32_kernel<P, false, true, 8, 4>
-                : variant == 5 ? ensf_f32_kernel<P, false, true, 0, 3, false, 256, false>
-                : ctas == 4    ? ensf_f32_kernel<P, false, true, 0, 4>
-                : ctas == 7    ? ensf_f32_kernel<P, false, true, 0, 7, false, 128>
-                : ctas == 2    ? ensf_f32_kernel<P, false, true, 0, 2>
-                               : ensf_f32_kernel<P, false, true, 0, 3>;
+template <class K>
+cudaError_t launch_kernel(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          const KernelArgs& a, const float* xt, const double2* ab,
+                          const StepF32* steps, const int32_t* batches, float* z,
+                          unsigned long long* status) {
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(smem));
@@ -755,6 +743,73 @@ cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab
     }
     kern<<<grid, block, smem, st>>>(a, xt, ab, steps, batches, z, status);
     return cudaGetLastError();
+}
+
+// Kernel choice (sweeps in profiles/):
+//  * sorted member tiles (N > 24), four tiles fit in shared memory: 8-warp
+//    CTAs, 4 per SM (64 registers), 1/8 of the exponentials on the FMA-pipe
+//    polynomial (config 2, config 5);
+//  * sorted, one tile per SM (N >~ 440, config 4): one 32-warp CTA per SM
+//    with the same 1/8 share;
+//  * sorted, two or three tiles fit: 8-warp CTAs, 3 per SM, all MUFU;
+//  * unsorted tiles (N <= 24, configs 1 and 3: brute-force redo shift):
+//    CTAs of ceil(N/P) warps, 64 registers, kPolyUnsorted share;
+//  * minibatches and ensembles whose tile exceeds shared memory: the
+//    two-pass member loop, all MUFU.
+constexpr int kPolySorted = 8;
+constexpr int kPolyUnsorted = 0;
+
+template <int P>
+cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab,
+                         const StepF32* steps, const int32_t* batches, float* z,
+                         unsigned long long* status, cudaStream_t st, bool sorted) {
+    static const int poly_env = env_int("TURBDA_F32_POLY", -1);
+    static const bool exact = env_int("TURBDA_F32_EXACT_SHIFT", 0) != 0;
+    const int groups = (a.m + P - 1) / P;
+    const bool global_x = f32_members_global(a.m);
+    const size_t smem = global_x ? 0 : sizeof(float2) * 32 * size_t(a.m);
+    const size_t smem_sm = size_t(227) * 1024;
+    const bool wide = sorted && !exact && smem * 2 > smem_sm;  // one tile per SM
+    const int wmax = wide ? 32 : 8;
+    const int nw = groups < wmax ? groups : wmax;
+    const dim3 block(32 * nw);
+    const dim3 grid(unsigned((a.dl + kTile - 1) / kTile), unsigned((groups + nw - 1) / nw));
+    auto go = [&](auto kern) {
+        return launch_kernel(kern, grid, block, smem, st, a, xt, ab, steps, batches, z, status);
+    };
+    if (global_x)
+        return a.minibatch ? go(ensf_f32_kernel<P, true, false, 0, 3, true>)
+                           : go(ensf_f32_kernel<P, false, false, 0, 3, true>);
+    if (a.minibatch) return go(ensf_f32_kernel<P, true, false, 0, 3>);
+    if (!sorted) {
+        if (exact) return go(ensf_f32_kernel<P, false, false, 0, 4, false, 256, false>);
+        static const int minb = env_int("TURBDA_F32_MINB", 4);
+        if (minb == 3) {
+            switch (poly_env >= 0 ? poly_env : kPolyUnsorted) {
+                case 8: return go(ensf_f32_kernel<P, false, false, 8, 3>);
+                case 5: return go(ensf_f32_kernel<P, false, false, 5, 3>);
+                case 4: return go(ensf_f32_kernel<P, false, false, 4, 3>);
+                default: return go(ensf_f32_kernel<P, false, false, 0, 3>);
+            }
+        }
+        switch (poly_env >= 0 ? poly_env : kPolyUnsorted) {
+            case 8: return go(ensf_f32_kernel<P, false, false, 8, 4>);
+            case 5: return go(ensf_f32_kernel<P, false, false, 5, 4>);
+            case 4: return go(ensf_f32_kernel<P, false, false, 4, 4>);
+            default: return go(ensf_f32_kernel<P, false, false, 0, 4>);
+        }
+    }
+    if (exact) return go(ensf_f32_kernel<P, false, true, 0, 3, false, 256, false>);
+    if (wide) return go(ensf_f32_kernel<P, false, true, kPolySorted, 1, false, 1024>);
+    if (smem * 4 <= smem_sm) {
+        switch (poly_env >= 0 ? poly_env : kPolySorted) {
+            case 5: return go(ensf_f32_kernel<P, false, true, 5, 4>);
+            case 4: return go(ensf_f32_kernel<P, false, true, 4, 4>);
+            case 0: return go(ensf_f32_kernel<P, false, true, 0, 4>);
+            default: return go(ensf_f32_kernel<P, false, true, 8, 4>);
+        }
+    }
+    return go(ensf_f32_kernel<P, false, true, 0, 3>);
 }
 
 template <int P, bool kSmemX>
@@ -765,8 +820,7 @@ cudaError_t launch_f64_p(const KernelArgs& a, const double* x, const double2* ab
     const int nw = groups < 4 ? groups : 4;
     const dim3 block(32 * nw);
     const dim3 grid(unsigned((a.dl + kTile - 1) / kTile), unsigned((groups + nw - 1) / nw));
-    const size_t smem = sizeof(StepF64) * size_t(a.n_steps) +
-                        (kSmemX ? sizeof(double2) * 32 * size_t(a.m) : 0);
+    const size_t smem = kSmemX ? sizeof(double2) * 32 * size_t(a.m) : 0;
     auto kern = a.minibatch ? ensf_f64_kernel<P, true, kSmemX> : ensf_f64_kernel<P, false, kSmemX>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -779,18 +833,51 @@ cudaError_t launch_f64_p(const KernelArgs& a, const double* x, const double2* ab
 
 }  // namespace
 
+size_t obs_prep_scratch_bytes(int64_t obs_dim) {
+    if (obs_dim <= 0) return 0;
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, static_cast<const int64_t*>(nullptr),
+                                    static_cast<int64_t*>(nullptr),
+                                    static_cast<const int32_t*>(nullptr),
+                                    static_cast<int32_t*>(nullptr), obs_dim);
+    const size_t n = size_t(obs_dim);
+    return align256(8 * n) + 2 * align256(4 * n) + align256(tmp);
+}
+
 cudaError_t launch_obs_prep(const double* y, const double* r, const int64_t* idx,
                             int64_t obs_dim, int obs_kind, int64_t k0, int64_t dl, double2* ab,
-                            cudaStream_t st, int64_t r_stride) {
+                            cudaStream_t st, int64_t r_stride, bool idx_increasing,
+                            void* scratch, size_t scratch_bytes) {
     if (dl <= 0) return cudaSuccess;
     if (obs_dense(obs_kind)) {
         obs_identity_kernel<<<blocks_for(dl, 256), 256, 0, st>>>(y, r, r_stride, dl, ab);
+        add_launches(1);
         return cudaGetLastError();
     }
     cudaError_t e = cudaMemsetAsync(ab, 0, sizeof(double2) * size_t(dl), st);
     if (e != cudaSuccess || obs_dim == 0) return e;
-    obs_select_kernel<<<blocks_for(obs_dim, 256), 256, 0, st>>>(y, r, r_stride, idx, obs_dim, k0,
-                                                                   dl, ab);
+    if (obs_dim > INT32_MAX) return cudaErrorInvalidValue;
+    if (idx_increasing) {
+        obs_select_unique_kernel<<<blocks_for(obs_dim, 256), 256, 0, st>>>(y, r, r_stride, idx,
+                                                                          obs_dim, k0, dl, ab);
+        add_launches(1);
+        return cudaGetLastError();
+    }
+    if (!scratch || scratch_bytes < obs_prep_scratch_bytes(obs_dim)) return cudaErrorInvalidValue;
+    const size_t n = size_t(obs_dim);
+    unsigned char* b = static_cast<unsigned char*>(scratch);
+    int64_t* keys = reinterpret_cast<int64_t*>(b);
+    int32_t* pos_in = reinterpret_cast<int32_t*>(b + align256(8 * n));
+    int32_t* pos = reinterpret_cast<int32_t*>(b + align256(8 * n) + align256(4 * n));
+    void* tmp = b + align256(8 * n) + 2 * align256(4 * n);
+    size_t tmp_bytes = scratch_bytes - (align256(8 * n) + 2 * align256(4 * n));
+    iota_kernel<<<blocks_for(obs_dim, 256), 256, 0, st>>>(pos_in, obs_dim);
+    // LSD radix sort is stable: equal indices keep observation order
+    e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, idx, keys, pos_in, pos, obs_dim, 0, 64, st);
+    if (e != cudaSuccess) return e;
+    obs_select_runs_kernel<<<blocks_for(obs_dim, 256), 256, 0, st>>>(y, r, r_stride, keys, pos,
+                                                                    obs_dim, k0, dl, ab);
+    add_launches(3);
     return cudaGetLastError();
 }
 
@@ -805,9 +892,7 @@ cudaError_t launch_ensf_f32(const KernelArgs& a, const double* x, const double2*
     const unsigned tiles = unsigned((a.dl + kTile - 1) / kTile);
     // sorted tiles + binary-searched shift pay off past ~24 members; below,
     // the brute-force min pass is cheaper (measured, configs 1 and 3)
-    const int variant = f32_variant();
-    const bool sorted = !a.minibatch && variant != 2 && (a.j_batch > 24 || variant == 3) &&
-                        !f32_members_global(a.m, a.n_steps);
+    const bool sorted = !a.minibatch && a.j_batch > 24 && !f32_members_global(a.m);
     const size_t smem = sizeof(float) * size_t(a.m) * kTile;
     if (sorted) {
         if (smem > 48 * 1024) {
@@ -827,13 +912,7 @@ cudaError_t launch_ensf_f32(const KernelArgs& a, const double* x, const double2*
     const auto warps_for = [&](int pp) { return tiles_n * ((a.m + pp - 1) / pp); };
     const int64_t wave = 148 * 24;
     // (particles past m in the last warp are computed and discarded)
-    static const int forced_p = [] {
-        const char* e = std::getenv("TURBDA_F32_P");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (forced_p == 4) return launch_f32_p<4>(a, xt, ab, steps, batches, z, status, st, sorted);
-    if (forced_p == 2) return launch_f32_p<2>(a, xt, ab, steps, batches, z, status, st, sorted);
-    if (forced_p == 1) return launch_f32_p<1>(a, xt, ab, steps, batches, z, status, st, sorted);
+    static const int forced_p = env_int("TURBDA_F32_P", 0);  // experiments
     if ((a.m % 4 == 0 || a.m >= 32) && warps_for(4) >= wave)
         return launch_f32_p<4>(a, xt, ab, steps, batches, z, status, st, sorted);
     if ((a.m % 2 == 0 || a.m >= 16) && warps_for(2) >= wave / 2)
@@ -877,13 +956,14 @@ cudaError_t launch_score_f64(const double* z, const double* x, int m, int64_t d,
     return cudaGetLastError();
 }
 
+size_t diag_scratch_doubles() { return 2 + 2 * size_t(kDiagBlocks); }
+
 cudaError_t launch_diag(const double* x, int m, int64_t d, const double* truth, double* out,
                         cudaStream_t st) {
-    cudaError_t e = cudaMemsetAsync(out, 0, 2 * sizeof(double), st);
-    if (e != cudaSuccess || d <= 0) return e;
-    int blocks = blocks_for(d, 256);
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    diag_kernel<<<blocks, 256, 0, st>>>(x, m, d, truth, out);
+    double* part = out + 2;
+    diag_kernel<<<kDiagBlocks, 256, 0, st>>>(x, m, d, truth, part);
+    sum_partials_kernel<<<1, 32, 0, st>>>(part, kDiagBlocks, out);
+    add_launches(2);
     return cudaGetLastError();
 }
 

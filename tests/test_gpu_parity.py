@@ -220,13 +220,13 @@ def test_far_from_members_exact_shift_redo(capi, port, m, minibatch, y0, r):
 
 def test_shift_free_weights_match_exact_shift_kernel(capi, tmp_path):
     """Default kernel (shift-free weight pass + per-value redo) vs the kernel
-    that always takes the exact shift first (TURBDA_F32_VARIANT=5 sorted,
-    =6 brute force; a fresh process, the variant is read once): the same
-    estimator to fp32 rounding."""
+    that always takes the exact shift first (TURBDA_F32_EXACT_SHIFT=1: sorted
+    tiles at N = 64, brute force at N = 20; a fresh process, the knob is read
+    once): the same estimator to fp32 rounding."""
     import os
     import subprocess
     import sys
-    for m, variant in ((64, 5), (20, 6)):
+    for m in (64, 20):
         x, y, idx = throughput_inputs(m, 4096, stride=4)
         np.save(tmp_path / "x.npy", x)
         np.save(tmp_path / "y.npy", y)
@@ -234,7 +234,7 @@ def test_shift_free_weights_match_exact_shift_kernel(capi, tmp_path):
         code = ("import numpy as np, sys; from paper_2407_12168_b200 import capi; "
                 "d = sys.argv[1]; x, y, i = (np.load(d + f) for f in ('/x.npy', '/y.npy', '/i.npy')); "
                 "np.save(d + '/out.npy', capi.analyze_host(x, y, 1.0, i, n_steps=100))")
-        env = dict(os.environ, TURBDA_F32_VARIANT=str(variant))
+        env = dict(os.environ, TURBDA_F32_EXACT_SHIFT="1")
         subprocess.run([sys.executable, "-c", code, str(tmp_path)], check=True, env=env,
                        cwd=str(Path(__file__).resolve().parents[1]))
         exact = np.load(tmp_path / "out.npy")
@@ -463,6 +463,7 @@ def test_joint_mode_multi_process_nccl(capi):
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert "JOINT_MULTIPROC_OK" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
     assert "SHARD_VERDICT_OK" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "EMPTY_WINDOW_OK" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
 
 
 def test_async_calls_on_two_streams_do_not_share_scratch(capi):

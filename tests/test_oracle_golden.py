@@ -103,3 +103,34 @@ def test_reference_oracle_reproduces_goldens(ref):
         idx = rec["idx"] if int(rec["obs_kind"]) == 1 else None
         got = ref.analyze(rec["x"], rec["y"], rec["r"], idx, workers=4, **kw)
         assert rel_l2(got, rec["out"]) < 1e-13
+
+
+def test_high_counter_word_normals_vs_reference_philox(port, ref):
+    """8-GPU weak scaling of config 3 (d_total = 1.34e8) draws normal
+    n = (s+1) d_total + k up to 1.4e10: Philox block q = n >> 1 >= 2^32 uses
+    the counter's high word (proj/src/rng.cpp:49-56).  No golden reaches it,
+    so the port's normals there are rebuilt from the reference's own
+    philox4x32 + the Box-Muller of proj/src/rng.cpp:67-84 (Python's math
+    module is the same libm) and must match bit for bit."""
+    import math
+    key64 = port.splitmix64(7 ^ port.splitmix64(6))  # RngStream(7, ensf_particles)
+    key = np.array([key64 & 0xFFFFFFFF, key64 >> 32], np.uint32)
+    d_total = 134_217_728
+    for cycle, i in [(1, 0), (3, 19), (1 << 31, 511)]:
+        entity = (cycle << 32) | i
+        for s, k in [(63, d_total - 2), (64, d_total - 4096), (99, 12345678), (99, d_total - 2)]:
+            n0 = (s + 1) * d_total + k
+            assert n0 >> 1 >= 1 << 32 or s < 64
+            got = port.stream_normals(7, 6, entity, 4, n0=n0)
+            want = []
+            for n in range(n0, n0 + 4):
+                q = n >> 1
+                w = [int(v) for v in ref.philox4x32(
+                    np.array([q & 0xFFFFFFFF, q >> 32, entity & 0xFFFFFFFF, entity >> 32],
+                             np.uint32), key)]
+                u1 = (float((w[0] | (w[1] << 32)) >> 11) + 0.5) * 2.0 ** -53
+                u2 = (float((w[2] | (w[3] << 32)) >> 11) + 0.5) * 2.0 ** -53
+                r = math.sqrt(-2.0 * math.log(u1))
+                a = 2.0 * 3.14159265358979323846 * u2
+                want.append(r * math.sin(a) if n & 1 else r * math.cos(a))
+            assert np.array_equal(got, np.array(want)), (cycle, i, s, k)

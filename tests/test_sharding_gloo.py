@@ -79,10 +79,27 @@ def test_bench_shard_observation_indices():
     spec = importlib.util.spec_from_file_location("bench", ROOT / "bench.py")
     bench = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(bench)
+    import torch
     d, stride = 1000, 4
-    for k0 in (0, 1000, 2000, 3000):
-        _, _, idx = bench.make_inputs(d, 2, stride, k0)
-        assert np.array_equal(idx, np.arange(k0, k0 + d)[np.arange(k0, k0 + d) % stride == 0])
+    for k0 in (0, 1000, 2000, 3000, 1001, 2003):
+        want = np.arange(k0, k0 + d)[np.arange(k0, k0 + d) % stride == 0]
+        _, y, idx = bench.make_inputs_host(d, 2, stride, k0)
+        assert np.array_equal(idx, want) and y.size == want.size
+        _, ty, _, tidx = bench.make_inputs_device(torch, torch.device("cpu"), d, 2, stride, k0, 1)
+        assert np.array_equal(tidx.numpy(), want) and ty.numel() == want.size
+    _, _, idx = bench.make_inputs_host(d, 2, 1, 0)
+    assert idx is None
+
+
+def test_bench_refuses_mismatched_world(tmp_path):
+    """bench.py prints no line when WORLD_SIZE differs from --gpus."""
+    import subprocess
+    import sys
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2"], env=env,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 2 and out.stdout.strip() == ""
+    assert "refusing" in out.stderr
 
 
 def _joint_worker(rank, world, port, result):

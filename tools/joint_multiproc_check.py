@@ -71,7 +71,7 @@ def main():
     dist.all_gather_object(verdicts, verdict)
     # rmse / spread partial sums over the shards
     truth = y
-    sums = capi.diag(x[:, lo:hi], truth[lo:hi], device=local)
+    sums = capi.diag(x[:, lo:hi], truth[lo:hi], device=local, sharded=True)
     if rank == 0:
         whole = None
         try:
@@ -84,6 +84,28 @@ def main():
         ok_d = all(abs(a - b) <= 1e-10 * abs(b) for a, b in zip(sums, want))
         print(f"verdicts {verdicts} whole {whole}; diag {sums} want {want}", flush=True)
         print("SHARD_VERDICT_OK" if ok_v and ok_d else "SHARD_VERDICT_FAIL", flush=True)
+    # an empty window (fewer tiles than ranks): rank 0 holds the whole state,
+    # the others none; the empty ranks must join every collective (the joint
+    # per-step allreduce and the verdict min-reduce) instead of returning
+    lo_e, hi_e = (0, d) if rank == 0 else (d, d)
+    part_e = capi.analyze_host(x[:, lo_e:hi_e], y[lo_e:hi_e], 4.0, None, n_steps=20, joint=True,
+                               device=local, k0=lo_e, d_total=d, precision=capi.FP64)
+    r_e = np.ones(d)
+    r_e[7] = 1e-9
+    verdict_e = None
+    try:
+        capi.analyze_host(x[:, lo_e:hi_e], y[lo_e:hi_e], r_e[lo_e:hi_e], None, n_steps=20,
+                          device=local, k0=lo_e, d_total=d, precision=capi.FP64)
+    except capi.TurbdaError as e:
+        verdict_e = (e.code, e.diverged_particle, e.diverged_step)
+    verdicts_e = [None] * world
+    dist.all_gather_object(verdicts_e, verdict_e)
+    if rank == 0:
+        ee = rel_l2(part_e, PortOracle().analyze(x, y, 4.0, None, n_steps=20, joint=True))
+        ok_e = ee <= 1e-9 and verdicts_e[0] is not None and verdicts_e[0][0] == capi.DIVERGED \
+            and all(v == verdicts_e[0] for v in verdicts_e)
+        print(f"empty windows: joint rel-L2 {ee:.3e}, verdicts {verdicts_e}", flush=True)
+        print("EMPTY_WINDOW_OK" if ok_e else "EMPTY_WINDOW_FAIL", flush=True)
     capi.comm_destroy(local)
     dist.barrier()
     dist.destroy_process_group()
