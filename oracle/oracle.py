@@ -352,10 +352,11 @@ def conditioned_inputs(m, d, oracle=None, stride=0):
 
 
 class RefCycleOracle:
-    """The reference's cycle driver and SQG model (proj/src/{osse,config,
-    forecast,sqg,spectral}.cpp + the hot path), unmodified, built against
-    cuFFTW (oracle/ref_cycle_shim.cpp).  Needs a GPU at run time, except
-    ``letkf_analyze`` (the Eigen-free LETKF restatement, CPU only)."""
+    """The reference's cycle driver, SQG model and LETKF (proj/src/{osse,
+    config,forecast,sqg,spectral,letkf}.cpp + the hot path), unmodified,
+    built against cuFFTW and the Eigen subset in oracle/ref_shadow/Eigen
+    (oracle/ref_cycle_shim.cpp).  Needs a GPU at run time for the model
+    (cuFFTW); ``letkf_analyze`` is CPU only."""
 
     kind = "reference"
 
@@ -401,8 +402,9 @@ class RefCycleOracle:
 
     def letkf_analyze(self, x, y, r, idx, nx, ny, cutoff_km=2000.0, domain_km=20000.0,
                       rtps_alpha=0.3, workers=0):
-        """The C++ LETKF restatement (oracle/letkf_restated.cpp) through the
-        reference's own Ensemble / Observation types; CPU only."""
+        """The reference's own letkf_analyze (proj/src/letkf.cpp:57-174, with
+        rtps_inflate :176-207) through its Ensemble / Observation types;
+        CPU only."""
         x = np.ascontiguousarray(x, np.float64)
         y = np.ascontiguousarray(y, np.float64)
         r = np.ascontiguousarray(np.broadcast_to(np.asarray(r, np.float64), y.shape))

@@ -8,8 +8,9 @@
 //   refc_nature_run     -> turbda::nature_run      proj/src/osse.cpp:101-135
 //   refc_snapshot_write -> turbda::write_snapshot  proj/src/snapshot.cpp:12-30
 //   refc_snapshot_read  -> turbda::read_snapshot   proj/src/snapshot.cpp:32-63
-//   refc_letkf_analyze  -> turbda::letkf_analyze   (restated without Eigen,
-//                          oracle/letkf_restated.cpp; the cycle driver's
+//   refc_letkf_analyze  -> turbda::letkf_analyze   (proj/src/letkf.cpp
+//                          unmodified over the Eigen subset in
+//                          oracle/ref_shadow/Eigen/Dense; the cycle driver's
 //                          "letkf" variant calls the same function)
 #include <cstdint>
 #include <cstring>

@@ -1,7 +1,11 @@
-"""GPU LETKF arm (csrc/letkf_kernels.cu) against the numpy restatement of
-proj/src/letkf.cpp (oracle/letkf_oracle.py) and the properties of the
-reference's own proj/tests/test_letkf.cpp.  Parity unpinned for this arm
-(the reference needs Eigen, absent here): fp64 agreement to rounding."""
+"""GPU LETKF arm (csrc/letkf_kernels.cu) against the reference's own
+letkf_analyze (proj/src/letkf.cpp compiled unmodified into
+oracle/_ref/libturbda_ref_cycle.so over the Eigen subset in
+oracle/ref_shadow/Eigen/Dense - Eigen itself is absent here), the numpy
+restatement (oracle/letkf_oracle.py, which also covers the arctan extension
+and explicit locations the reference's API does not take) and the
+properties of the reference's own proj/tests/test_letkf.cpp.  fp64
+agreement to rounding (1e-9)."""
 from __future__ import annotations
 
 import numpy as np
@@ -49,6 +53,34 @@ def test_letkf_vs_restatement(capi, n, m, stride, arctan, cutoff, alpha):
     got = capi.letkf_analyze(x, y, r, idx, nx=n, ny=n, cutoff_km=cutoff, rtps_alpha=alpha,
                              arctan=arctan)
     want = L.letkf_analyze(x, y, r, idx, n, n, cutoff_km=cutoff, rtps_alpha=alpha, arctan=arctan)
+    assert rel_err(got, want) < TOL
+
+
+@pytest.mark.parametrize("n,m,stride,cutoff,alpha", [
+    (8, 6, 0, 2000.0, 0.3),
+    (16, 20, 3, 2000.0, 0.3),
+    (32, 33, 4, 2000.0, 0.5),
+    (64, 20, 4, 2000.0, 0.3),
+    (16, 128, 2, 2500.0, 0.3),
+    (256, 64, 4, 2000.0, 0.3),          # BASELINE config 2's grid and ensemble
+])
+def test_letkf_vs_reference(capi, n, m, stride, cutoff, alpha):
+    """The reference's letkf.cpp itself (proj/src/letkf.cpp:57-207)."""
+    from conftest import ROOT
+    from oracle.oracle import RefCycleOracle
+    path = ROOT / "oracle" / "_ref" / "libturbda_ref_cycle.so"
+    if not path.exists():
+        pytest.skip("oracle/_ref/libturbda_ref_cycle.so not built")
+    d = 2 * n * n
+    x = ens(m, d, 100 + n + m)
+    idx = None if stride == 0 else np.arange(0, d, stride, dtype=np.int64)
+    nobs = d if idx is None else idx.size
+    g = np.random.default_rng(7)
+    y = 0.3 + g.standard_normal(nobs)
+    r = 0.5 + g.random(nobs)
+    got = capi.letkf_analyze(x, y, r, idx, nx=n, ny=n, cutoff_km=cutoff, rtps_alpha=alpha)
+    want = RefCycleOracle(path).letkf_analyze(x, y, r, idx, n, n, cutoff_km=cutoff,
+                                              rtps_alpha=alpha)
     assert rel_err(got, want) < TOL
 
 

@@ -1,7 +1,8 @@
 """CPU: the numpy LETKF restatement (oracle/letkf_oracle.py) against the
 closed forms and properties of the reference's own proj/tests/test_letkf.cpp
-(the reference needs Eigen, absent here, so these cases are what pins the
-restatement).  Small grids: the restatement loops over grid points."""
+and against the reference's letkf.cpp itself (compiled unmodified over the
+Eigen subset in oracle/ref_shadow/Eigen/Dense - Eigen is absent here).
+Small grids: the restatement loops over grid points."""
 from __future__ import annotations
 
 import math
@@ -144,9 +145,9 @@ def _refcycle():
     (8, 6, 0, 2000.0, 0.3), (16, 20, 3, 2000.0, 0.0), (16, 9, 0, 1e12, 0.5), (32, 12, 4, 3000.0, 0.3),
 ])
 def test_two_restatements_agree(n, m, stride, cutoff, alpha):
-    """numpy (per point, reference gather order) vs the Eigen-free C++
-    restatement running inside the reference's own types and parallel_for
-    (periodic-stencil gather order, Jacobi eigensolver)."""
+    """numpy restatement (per point, reference gather order) vs the
+    reference's own letkf_analyze (proj/src/letkf.cpp, unmodified; Eigen's
+    SelfAdjointEigenSolver restated as cyclic Jacobi in the shadow header)."""
     rc = _refcycle()
     d = 2 * n * n
     x = gaussian_ensemble(m, d, 3 + n)
@@ -158,6 +159,6 @@ def test_two_restatements_agree(n, m, stride, cutoff, alpha):
     a = L.letkf_analyze(x, y, r, idx, n, n, cutoff_km=cutoff, rtps_alpha=alpha)
     b = rc.letkf_analyze(x, y, r, idx, n, n, cutoff_km=cutoff, rtps_alpha=alpha, workers=4)
     assert np.abs(a - b).max() <= 1e-10 * np.abs(a).max()
-    # the C++ restatement is bitwise independent of the worker count
+    # the reference is bitwise independent of the worker count
     assert np.array_equal(b, rc.letkf_analyze(x, y, r, idx, n, n, cutoff_km=cutoff,
                                               rtps_alpha=alpha, workers=1))
