@@ -296,6 +296,26 @@ TURBDA_API int turbda_run_experiment(const turbda_experiment* e, int32_t device,
                           int32_t max_records, int32_t* n_records, double* max_cfl,
                           double* phase_seconds, turbda_status* status);
 
+/* Open-loop probe of a cycled run: the same experiment, and at each listed
+ * cycle a copy of what that cycle's analysis saw and produced over the
+ * coordinate window [k0, k0 + width): the forecast ensemble, the analysis
+ * ensemble (both [n_cycles][m][width]) and the whole observation vector
+ * ([n_cycles][obs_dim]).  Lets a test recompute one cycle's analysis of the
+ * window with the CPU oracle and compare (open-loop per-cycle parity). */
+typedef struct turbda_probe {
+    int32_t n_cycles;
+    const int32_t* cycles;  /* ascending cycle numbers (1-based)              */
+    int64_t k0, width;      /* coordinate window                              */
+    double* forecast;       /* host, [n_cycles][ensemble_size][width]         */
+    double* analysis;       /* host, [n_cycles][ensemble_size][width]         */
+    double* y;              /* host, [n_cycles][obs_dim] (NULL: not copied)   */
+} turbda_probe;
+
+TURBDA_API int turbda_run_experiment_probe(const turbda_experiment* e, int32_t device,
+                                double* records, int32_t max_records, int32_t* n_records,
+                                double* max_cfl, double* phase_seconds,
+                                const turbda_probe* probe, turbda_status* status);
+
 /* -------------------------------------------------------------------------
  * LETKF arm: letkf_analyze / rtps_inflate /
  * gaspari_cohn, proj/include/turbda/letkf.hpp:11-56, proj/src/letkf.cpp:10-207.

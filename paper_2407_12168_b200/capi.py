@@ -481,6 +481,41 @@ def run_experiment_raw(e: Experiment, device=-1, phases=None):
     return rec[: n.value], cfl.value
 
 
+class Probe(C.Structure):
+    _fields_ = [("n_cycles", C.c_int32), ("cycles", C.c_void_p), ("k0", C.c_int64),
+                ("width", C.c_int64), ("forecast", C.c_void_p), ("analysis", C.c_void_p),
+                ("y", C.c_void_p)]
+
+
+def run_experiment_probe(e: Experiment, cycles, k0: int, width: int, obs_dim: int, device=-1):
+    """The experiment plus an open-loop probe (turbda_run_experiment_probe):
+    returns (records, {cycle: (forecast [m][width], analysis [m][width],
+    y [obs_dim])}) for the listed cycles."""
+    L = lib()
+    if not hasattr(L, "_probe_bound"):
+        L.turbda_run_experiment_probe.argtypes = [C.POINTER(Experiment), C.c_int32, C.c_void_p,
+                                                  C.c_int32, C.POINTER(C.c_int32),
+                                                  C.POINTER(C.c_double), C.c_void_p,
+                                                  C.POINTER(Probe), C.POINTER(Status)]
+        L.turbda_run_experiment_probe.restype = C.c_int
+        L._probe_bound = True
+    cyc = np.ascontiguousarray(sorted(cycles), np.int32)
+    m = e.ensemble_size
+    fc = np.zeros((cyc.size, m, width))
+    an = np.zeros((cyc.size, m, width))
+    yy = np.zeros((cyc.size, obs_dim))
+    pr = Probe(int(cyc.size), cyc.ctypes.data, int(k0), int(width), fc.ctypes.data,
+               an.ctypes.data, yy.ctypes.data)
+    rec = np.zeros((max(e.cycles, 1), 6), np.float64)
+    n = C.c_int32(0)
+    cfl = C.c_double(0)
+    st = Status()
+    _check(L.turbda_run_experiment_probe(C.byref(e), device, rec.ctypes.data, e.cycles,
+                                         C.byref(n), C.byref(cfl), None, C.byref(pr),
+                                         C.byref(st)), st)
+    return rec[: n.value], {int(c): (fc[q], an[q], yy[q]) for q, c in enumerate(cyc)}
+
+
 def device_count() -> int:
     return int(lib().turbda_device_count())
 

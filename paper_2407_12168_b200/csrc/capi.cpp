@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <condition_variable>
+#include <functional>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -64,6 +66,113 @@ int cuda_fail(turbda_status* st, cudaError_t e, const char* where) {
         if (e_ != cudaSuccess) return cuda_fail(st, e_, #call); \
     } while (0)
 
+// Host copy pool for pageable buffers: the CUDA driver stages pageable
+// memory through one internal pinned buffer on the calling thread (~9 GB/s
+// measured on the B200 host); the analysis instead gathers each chunk into
+// its own pinned slot with all pool threads and DMAs from there at the pinned
+// rate, and scatters results (incl. first-touch page faults of a fresh
+// output array) the same way.
+class CopyPool {
+public:
+    static CopyPool& get() {
+        static CopyPool pool;
+        return pool;
+    }
+    // fn(t) for t in [0, n), spread over the pool; returns when all are done
+    void run(int64_t n, const std::function<void(int64_t)>& fn) {
+        if (n <= 0) return;
+        std::unique_lock<std::mutex> lk(run_mu_);  // one parallel region at a time
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            fn_ = &fn;
+            n_ = n;
+            next_ = 0;
+            done_ = 0;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> g(mu_);
+        done_cv_.wait(g, [&] { return done_ == n_; });
+        fn_ = nullptr;
+    }
+
+private:
+    CopyPool() {
+        const unsigned hw = std::thread::hardware_concurrency();
+        const int nt = int(std::min<unsigned>(16, hw > 1 ? hw - 1 : 1));
+        for (int t = 0; t < nt; ++t)
+            std::thread([this] {
+                uint64_t seen = 0;
+                for (;;) {
+                    {
+                        std::unique_lock<std::mutex> g(mu_);
+                        cv_.wait(g, [&] { return gen_ != seen; });
+                        seen = gen_;
+                    }
+                    work();
+                }
+            }).detach();
+    }
+    void work() {
+        for (;;) {
+            int64_t t;
+            const std::function<void(int64_t)>* fn;
+            {
+                std::lock_guard<std::mutex> g(mu_);
+                if (!fn_ || next_ >= n_) return;
+                t = next_++;
+                fn = fn_;
+            }
+            (*fn)(t);
+            std::lock_guard<std::mutex> g(mu_);
+            if (++done_ == n_) done_cv_.notify_all();
+        }
+    }
+    std::mutex run_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(int64_t)>* fn_ = nullptr;
+    int64_t n_ = 0, next_ = 0, done_ = 0;
+    uint64_t gen_ = 0;
+};
+
+// m rows of `len` doubles between a row-pitched (or row-pointer) array and a
+// contiguous [m][len] block, in ~1 MB pieces over the copy pool
+void parallel_rows(int m, int64_t len, const std::function<void(int, int64_t, int64_t)>& piece) {
+    const int64_t step = std::max<int64_t>(int64_t(1) << 17, 1);  // 1 MB of doubles
+    const int64_t per_row = (len + step - 1) / step;
+    CopyPool::get().run(int64_t(m) * per_row, [&](int64_t t) {
+        const int j = int(t / per_row);
+        const int64_t lo = (t % per_row) * step;
+        piece(j, lo, std::min(len, lo + step) - lo);
+    });
+}
+
+bool pageable(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return at.type == cudaMemoryTypeUnregistered;
+}
+
+// Pinned host buffer that only grows.
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocDefault);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    double* d() const { return static_cast<double*>(p); }
+};
+
 // Device buffer that only grows.
 struct DevBuf {
     void* p = nullptr;
@@ -89,12 +198,16 @@ struct Workspace {
     cudaStream_t stream = nullptr;
     DevBuf x, z, xt, ab, steps, batches, status, out, y, r, idx;
     DevBuf obs_tmp, diag;                       // obs sort scratch, diag partials
+    DevBuf ticket;                              // fused fp32 kernel: per-tile tickets
     unsigned long long* status_host = nullptr;  // pinned
     void* comm = nullptr;                       // ncclComm_t (joint mode, sharded)
     int comm_world = 1;
     DevBuf jpart, jred, jw;                     // joint-mode scratch
     std::vector<cudaStream_t> cstreams;         // host-mode chunk pipeline
     std::vector<cudaEvent_t> ev_chunk;
+    static constexpr int kSlots = 3;            // pageable staging ring
+    PinnedBuf stage_in[kSlots], stage_out[kSlots];
+    cudaEvent_t ev_out[kSlots] = {};
     cudaEvent_t ev_ready = nullptr;
     // the scratch above is shared by every call on this device: an
     // asynchronous call leaves its stream here and its completion in ev_done
@@ -127,6 +240,7 @@ int ws_init(Workspace* w, turbda_status* st) {
         TB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&w->status_host), 64));
         TB_CUDA(cudaEventCreateWithFlags(&w->ev_ready, cudaEventDisableTiming));
         TB_CUDA(cudaEventCreateWithFlags(&w->ev_done, cudaEventDisableTiming));
+        for (cudaEvent_t& e : w->ev_out) TB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     return TURBDA_OK;
 }
@@ -423,14 +537,44 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
     }
     const int nc = int(chunks.size());
     if (int rc = ws_streams(w, nc, st)) return rc;
+    // pageable host arrays above 32 MB go through the pinned staging ring
+    constexpr int K = Workspace::kSlots;
+    const bool staged =
+        !on_dev && md * sizeof(double) >= (size_t(32) << 20) &&
+        (pageable(frows ? static_cast<const void*>(frows[0]) : forecast) ||
+         pageable(orows ? static_cast<const void*>(orows[0]) : out));
+    if (staged) {
+        size_t slot_bytes = 0;
+        for (const Window& c : chunks) slot_bytes = std::max(slot_bytes, sizeof(double) * size_t(m) * size_t(c.dl));
+        for (int q = 0; q < K; ++q) {
+            TB_CUDA(w->stage_in[q].reserve(slot_bytes));
+            TB_CUDA(w->stage_out[q].reserve(slot_bytes));
+        }
+    }
+    // staged: results of chunk q leave the ring once its D2H has finished
+    const auto drain = [&](int q) -> int {
+        const Window& c = chunks[size_t(q)];
+        if (c.dl <= 0 || m <= 0) return TURBDA_OK;
+        TB_CUDA(cudaEventSynchronize(w->ev_out[q % K]));
+        const double* src = w->stage_out[q % K].d();
+        const int64_t col = win.k0_local + c.k0_local;
+        parallel_rows(m, c.dl, [&](int j, int64_t lo, int64_t n) {
+            double* dst = orows ? orows[j] + col : out + size_t(j) * size_t(p->d_local) + size_t(col);
+            std::memcpy(dst + lo, src + size_t(j) * size_t(c.dl) + size_t(lo), sizeof(double) * size_t(n));
+        });
+        return TURBDA_OK;
+    };
 
     // scratch: every chunk owns a disjoint region
-    size_t xt_total = 0;
-    std::vector<size_t> xt_off;
+    size_t xt_total = 0, tk_total = 0;
+    std::vector<size_t> xt_off, tk_off;
     for (const Window& c : chunks) {
         xt_off.push_back(xt_total);
+        tk_off.push_back(tk_total);
         xt_total += fp32 ? ensf_f32_scratch_bytes(m, c.dl) : 0;
+        tk_total += fp32 ? ensf_f32_ticket_bytes(c.dl) : 0;
     }
+    TB_CUDA(w->ticket.reserve(std::max<size_t>(tk_total, 1)));
     TB_CUDA(w->z.reserve((fp32 ? sizeof(float) : sizeof(double)) * std::max<size_t>(md, 1)));
     TB_CUDA(w->xt.reserve(std::max<size_t>(xt_total, 1)));
     TB_CUDA(w->ab.reserve(sizeof(double2) * size_t(std::max<int64_t>(dl, 1))));
@@ -503,7 +647,21 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
         const int64_t col = win.k0_local + c.k0_local;  // column in the caller's arrays
         if (!on_dev) {
             TB_CUDA(cudaStreamWaitEvent(cs, w->ev_ready, 0));
-            if (c.dl > 0 && m > 0) {
+            if (staged && c.dl > 0 && m > 0) {
+                // the slot's previous chunk (q - K) must have left the ring
+                if (q >= K)
+                    if (int rc = drain(q - K)) return rc;
+                double* slot = w->stage_in[q % K].d();
+                parallel_rows(m, c.dl, [&](int j, int64_t lo, int64_t n) {
+                    const double* src = frows ? frows[j] + col
+                                              : forecast + size_t(j) * size_t(p->d_local) + size_t(col);
+                    std::memcpy(slot + size_t(j) * size_t(c.dl) + size_t(lo), src + lo,
+                                sizeof(double) * size_t(n));
+                });
+                TB_CUDA(cudaMemcpyAsync(w->x.as<double>() + moff, slot,
+                                        sizeof(double) * size_t(m) * size_t(c.dl),
+                                        cudaMemcpyHostToDevice, cs));
+            } else if (c.dl > 0 && m > 0) {
                 if (frows) {
                     for (int j = 0; j < m; ++j)
                         TB_CUDA(cudaMemcpyAsync(w->x.as<double>() + moff + size_t(j) * size_t(c.dl),
@@ -534,12 +692,17 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
         a.dl = c.dl;
         if (prof.a) TB_CUDA(cudaEventRecord(prof.a, cs));
         if (fp32) {
+            // one fused launch: tiles, every pseudo-step, relax_spread
+            a.x64 = dx;
+            a.out64 = dout;
+            a.relax = p->relax_factor;
+            a.tile_ticket = reinterpret_cast<unsigned int*>(w->ticket.as<unsigned char>() +
+                                                            tk_off[size_t(q)]);
             float* zc = w->z.as<float>() + moff;
-            TB_CUDA(launch_ensf_f32(a, dx, abc, w->steps.as<StepF32>(), w->batches.as<int32_t>(),
+            TB_CUDA(launch_ensf_f32(a, abc, w->steps.as<StepF32>(), w->batches.as<int32_t>(),
                                     reinterpret_cast<float*>(w->xt.as<unsigned char>() + xt_off[size_t(q)]),
                                     zc, dstatus, cs, dl));
             if (prof.b) TB_CUDA(cudaEventRecord(prof.b, cs));
-            TB_CUDA(launch_relax_f32(zc, dx, m, c.dl, p->relax_factor, dout, cs));
         } else {
             double* zc = w->z.as<double>() + moff;
             TB_CUDA(launch_ensf_f64(a, dx, abc, w->steps.as<StepF64>(), w->batches.as<int32_t>(),
@@ -547,7 +710,12 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
             if (prof.b) TB_CUDA(cudaEventRecord(prof.b, cs));
             TB_CUDA(launch_relax_f64(zc, dx, m, c.dl, p->relax_factor, dout, cs));
         }
-        g_launches += fp32 ? 3 : 2;
+        if (staged && c.dl > 0 && m > 0) {
+            TB_CUDA(cudaMemcpyAsync(w->stage_out[q % K].p, dout, sizeof(double) * size_t(m) * size_t(c.dl),
+                                    cudaMemcpyDeviceToHost, cs));
+            TB_CUDA(cudaEventRecord(w->ev_out[q % K], cs));
+        }
+        if (!fp32) g_launches += 2;  // (the fp32 path counts its own launches)
     }
     if (prof.a) {
         std::lock_guard<std::mutex> lk2(g_prof_mu);
@@ -563,10 +731,13 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
         return TURBDA_OK;
     }
 
+    if (staged)
+        for (int q = std::max(0, nc - K); q < nc; ++q)
+            if (int rc = drain(q)) return rc;
     if (!on_dev) {
         // results back per chunk, in chunk order (for pageable destinations
         // each copy returns once its chunk is done; later chunks keep running)
-        for (int q = 0; q < nc; ++q) {
+        for (int q = 0; q < nc && !staged; ++q) {
             const Window& c = chunks[size_t(q)];
             if (c.dl <= 0 || m <= 0) continue;
             cudaStream_t cs = w->cstreams[size_t(q)];

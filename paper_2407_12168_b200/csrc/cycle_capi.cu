@@ -442,6 +442,14 @@ void turbda_experiment_init(turbda_experiment* e) {
 int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* records,
                           int32_t max_records, int32_t* n_records, double* max_cfl,
                           double* phase_seconds, turbda_status* st) {
+    return turbda_run_experiment_probe(e, device, records, max_records, n_records, max_cfl,
+                                       phase_seconds, nullptr, st);
+}
+
+int turbda_run_experiment_probe(const turbda_experiment* e, int32_t device, double* records,
+                                int32_t max_records, int32_t* n_records, double* max_cfl,
+                                double* phase_seconds, const turbda_probe* probe,
+                                turbda_status* st) {
     clear(st);
     *n_records = 0;
     if (phase_seconds)
@@ -482,6 +490,11 @@ int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* re
     if (e->clim_hours < 0.0) return fail(st, TURBDA_CONFIG, "clim_hours >= 0");
     const int n_clim = int(std::llround(e->clim_hours / e->obs_interval)) + 1;
     if (e->ensemble_size > n_clim) return fail(st, TURBDA_CONFIG, "climatology too short for ensemble_size");
+    if (probe && (probe->n_cycles < 0 || (probe->n_cycles > 0 && (!probe->cycles || !probe->forecast ||
+                                                                 !probe->analysis)) ||
+                  probe->k0 < 0 || probe->width < 0 ||
+                  probe->k0 + probe->width > int64_t(2) * e->sqg.nx * e->sqg.ny))
+        return fail(st, TURBDA_CONFIG, "probe: window outside the state");
 
     if (device >= 0) CY_CUDA(cudaSetDevice(device));
     int dev = 0;
@@ -678,6 +691,22 @@ int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* re
                 uint32_t(obs_key >> 32), uint64_t(k), dy.as<double>());
             CY_CUDA(cudaGetLastError());
             ap.cycle = uint64_t(k);
+            // open-loop probe: this cycle's forecast window and observations
+            int slot = -1;
+            if (probe)
+                for (int q = 0; q < probe->n_cycles; ++q)
+                    if (probe->cycles[q] == k) slot = q;
+            const size_t pw = probe ? size_t(probe->width) : 0;
+            if (slot >= 0) {
+                CY_CUDA(cudaMemcpy2DAsync(probe->forecast + size_t(slot) * size_t(m) * pw,
+                                          sizeof(double) * pw, ens.as<double>() + probe->k0,
+                                          sizeof(double) * size_t(d), sizeof(double) * pw,
+                                          size_t(m), cudaMemcpyDeviceToHost, s));
+                if (probe->y)
+                    CY_CUDA(cudaMemcpyAsync(probe->y + size_t(slot) * size_t(nobs), dy.p,
+                                            sizeof(double) * size_t(nobs), cudaMemcpyDeviceToHost,
+                                            s));
+            }
             turbda_status ast{};
             const int rc =
                 e->variant == TURBDA_VARIANT_LETKF
@@ -686,6 +715,13 @@ int turbda_run_experiment(const turbda_experiment* e, int32_t device, double* re
                     : turbda_ensf_analyze(&ap, ens.as<double>(), dy.as<double>(), dr.as<double>(),
                                           didx.as<int64_t>(), ens_out.as<double>(), s, &ast);
             if (rc != TURBDA_OK) return aborted(k, ast.msg);
+            if (slot >= 0) {
+                CY_CUDA(cudaMemcpy2DAsync(probe->analysis + size_t(slot) * size_t(m) * pw,
+                                          sizeof(double) * pw, ens_out.as<double>() + probe->k0,
+                                          sizeof(double) * size_t(d), sizeof(double) * pw,
+                                          size_t(m), cudaMemcpyDeviceToHost, s));
+                CY_CUDA(cudaStreamSynchronize(s));
+            }
             toc(2);
             std::swap(ens.p, ens_out.p);
             tic();

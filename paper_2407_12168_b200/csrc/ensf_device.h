@@ -43,6 +43,12 @@ struct KernelArgs {
     uint32_t cycle_lo;    // entity = (cycle << 32) | i  ->  hi word
     int32_t obs_atan;     // 1: h(x) = atan(x) (obs kinds 2, 3), 0: linear
     PhiloxKeys rk;        // round keys of (key0, key1)
+    // fp32 analysis: the window's fp64 forecast [m][dl], the fp64 analysis
+    // [m][dl] and relax_spread's factor (read by the fused kernel)
+    const double* x64;
+    double* out64;
+    double relax;
+    unsigned int* tile_ticket;  // fused, several CTAs per tile: [tiles] zeros
 };
 
 // observation operator kinds of the C-ABI (include/turbda_b200.h)
@@ -62,15 +68,19 @@ cudaError_t launch_obs_prep(const double* y, const double* r, const int64_t* idx
                             double2* ab, cudaStream_t st, int64_t r_stride,
                             bool idx_increasing, void* scratch, size_t scratch_bytes);
 
-// full fused analysis into z (fp32 or fp64 scratch, [m][dl]).  The fp32 path
-// first converts (and, without minibatches, sorts per coordinate) the
-// forecast into fp32 tiles `xt` of ensf_f32_scratch_bytes(m, dl) bytes.
+// fp32 analysis of a window: forecast a.x64 -> analysis a.out64 (fp64,
+// [m][dl]) including relax_spread (a.relax).  Normally ONE fused launch
+// (tile conversion/sort, all pseudo-steps, relax epilogue over a cluster of
+// the tile's CTAs); minibatches, ensembles whose tile exceeds shared memory
+// and the exact-shift cross-check run prep_tiles -> ensf_f32 -> relax with
+// the fp32 tiles in `xt` (ensf_f32_scratch_bytes) and particles in `z`.
 size_t ensf_f32_scratch_bytes(int m, int64_t dl);
+inline size_t ensf_f32_ticket_bytes(int64_t dl) { return sizeof(unsigned int) * size_t((dl + 63) / 64 + 1); }
 // dl_concurrent: coordinates analysed concurrently with this launch (the
 // whole call when the host pipeline runs chunks side by side; 0 = a.dl),
 // which sets the particles-per-warp choice.
-cudaError_t launch_ensf_f32(const KernelArgs& a, const double* x, const double2* ab,
-                            const StepF32* steps, const int32_t* batches, float* xt, float* z,
+cudaError_t launch_ensf_f32(const KernelArgs& a, const double2* ab, const StepF32* steps,
+                            const int32_t* batches, float* xt, float* z,
                             unsigned long long* status, cudaStream_t st,
                             int64_t dl_concurrent = 0);
 cudaError_t launch_ensf_f64(const KernelArgs& a, const double* x, const double2* ab,

@@ -43,10 +43,21 @@ __device__ __forceinline__ float ex2f(float x) {
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
-__device__ __forceinline__ float rcp_approx(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
+// num / den per coordinate.  kNewton (default): 1 / den on the FMA pipe -
+// the 0x7EF311C3 seed (rel. error < 1/8) and three Newton steps
+// r <- r (2 - den r) (rel. error < 1e-7), packed over the pair (config 3:
+// 192.0 ms vs 195.1 ms with MUFU.RCP, profiles/r02_sweeps.md); otherwise
+// MUFU.RCP (__fdividef).  den lies in [2^-60, J] (the redo guarantees the
+// lower bound); a non-finite den only occurs in a diverged run.
+template <bool kNewton>
+__device__ __forceinline__ float2 recip_mul(float2 num, float2 den) {
+    if (!kNewton) return make_float2(__fdividef(num.x, den.x), __fdividef(num.y, den.y));
+    float2 r = make_float2(__uint_as_float(0x7EF311C3u - __float_as_uint(den.x)),
+                           __uint_as_float(0x7EF311C3u - __float_as_uint(den.y)));
+    const float2 nd = make_float2(-den.x, -den.y);
+#pragma unroll
+    for (int it = 0; it < 3; ++it) r = __fmul2_rn(r, __ffma2_rn(nd, r, f2(2.f)));
+    return __fmul2_rn(num, r);
 }
 
 // one pseudo-step's coefficients: a warp-uniform 32 B read (L1 broadcast)
@@ -164,13 +175,208 @@ __device__ __forceinline__ void nearest_abs_u(const float* __restrict__ xsf, int
 // NaN sorts last so every column stays a permutation of its members.
 __device__ __forceinline__ float sort_key(float v) { return v != v ? __int_as_float(0x7f800000) : v; }
 
+constexpr int kSortWarps = 8;  // warps that sort the fused tile's columns
+
+// Fused prologue: the tile's forecast [m][64] (fp64, coalesced 512 B member
+// rows) -> fp32 in shared memory, zero padded past dl; for kSorted every
+// column sorted ascending (NaN last, ties by member index: the rank of
+// (j, c) counts the members that order before it, so the column stays a
+// permutation) by up to kSortWarps warps, one column at a time through a
+// per-warp staging column.  The forecast statistics of relax_spread
+// (ensemble_mean, proj/src/ensemble.cpp:7-16, then the sum of squared
+// deviations, proj/src/ensf.cpp:225-258) in fp64 and member order, exactly
+// as relax_kernel takes them.
+template <bool kSorted>
+__device__ __forceinline__ void fused_prologue(const KernelArgs& a, float* tile, int64_t tile0,
+                                               double2* fstat) {
+    const int m = a.m;
+    // pairs of coordinates (16 B loads when the rows are 16-byte aligned),
+    // unrolled so each thread keeps several loads in flight
+    const bool vec = ((a.dl & 1) == 0) && ((reinterpret_cast<uintptr_t>(a.x64) & 15) == 0);
+#pragma unroll 4
+    for (int q = threadIdx.x; q < m * (kTile / 2); q += blockDim.x) {
+        const int j = q >> 5, c = 2 * (q & 31);
+        const int64_t k = tile0 + c;
+        const double* src = a.x64 + size_t(j) * size_t(a.dl) + size_t(k);
+        double2 v = make_double2(0.0, 0.0);
+        if (k + 1 < a.dl) {
+            v = vec ? __ldg(reinterpret_cast<const double2*>(src)) : make_double2(__ldg(src), __ldg(src + 1));
+        } else if (k < a.dl) {
+            v.x = __ldg(src);
+        }
+        *reinterpret_cast<float2*>(tile + j * kTile + c) = make_float2(float(v.x), float(v.y));
+    }
+    if (threadIdx.x < kTile) {
+        const int64_t k = tile0 + threadIdx.x;
+        double mb = 0.0, sb = 0.0;
+        if (k < a.dl && a.relax != 0.0 && m >= 2) {
+            // member-order sums; the loads are batched 8 ahead of the adds
+            const double* col = a.x64 + size_t(k);
+            const size_t ld = size_t(a.dl);
+#pragma unroll 8
+            for (int j = 0; j < m; ++j) mb += __ldg(col + size_t(j) * ld);
+            mb *= 1.0 / m;
+            double vb = 0.0;
+#pragma unroll 8
+            for (int j = 0; j < m; ++j) {
+                const double db = __ldg(col + size_t(j) * ld) - mb;
+                vb += db * db;
+            }
+            sb = sqrt(vb / (m - 1));
+        }
+        fstat[threadIdx.x] = make_double2(mb, sb);
+    }
+    __syncthreads();
+    if (!kSorted) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sorters = min(int(blockDim.x >> 5), kSortWarps);
+    float* stage = tile + size_t(m) * kTile + size_t(warp) * size_t(m);  // [m] per warp
+    if (warp < sorters) {
+        for (int c = warp; c < kTile; c += sorters) {
+            for (int j = lane; j < m; j += 32) stage[j] = tile[j * kTile + c];
+            __syncwarp();
+            for (int j = lane; j < m; j += 32) {
+                const float v = stage[j];
+                const float kv = sort_key(v);
+                int rank = 0;
+                for (int i = 0; i < m; ++i) {
+                    const float ki = sort_key(stage[i]);
+                    rank += (ki < kv) || (ki == kv && i < j);
+                }
+                tile[rank * kTile + c] = v;
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+}
+
+// Fused epilogue: relax_spread of the tile (proj/src/ensf.cpp:225-258).
+// One CTA per tile (grid.y == 1): the particles go to shared memory (the
+// member tile is dead by now).  Several CTAs per tile: each writes its
+// particles to the fp32 scratch `zg` ([m][dl]) and takes a ticket; the last
+// CTA of the tile to finish relaxes the whole tile from there (L2-resident)
+// - no co-scheduling constraint, unlike a thread-block cluster, which
+// measured 6 % slower at N = 128 (profiles/r02_sweeps.md).  Either way one
+// thread per coordinate sums every particle in member order, so ma / va are
+// the reference's sequential fp64 sums (bit-identical to relax_kernel), and
+// the fp64 analysis is written once.  relax_factor 0 or one member: the
+// analysis is the particles themselves.
+template <int P>
+__device__ __forceinline__ void fused_relax_epilogue(const KernelArgs& a, float* zs, float* zg,
+                                                     int64_t tile0, int64_t kl, int i0,
+                                                     const double2* fstat, const float2 (&z)[P]) {
+    __shared__ double2 rstat[kTile];  // (ma, scale)
+    __shared__ unsigned int ticket;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool relax = a.relax != 0.0 && a.m >= 2;
+    const bool shared_path = gridDim.y == 1;
+    const bool aligned = (a.dl & 1) == 0;
+    __syncthreads();  // every warp is done with the member tile
+    if (shared_path) {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int il = warp * P + p;
+            zs[il * kTile + 2 * lane] = z[p].x;
+            zs[il * kTile + 2 * lane + 1] = z[p].y;
+        }
+    } else {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int i = i0 + p;
+            if (i >= a.m) continue;
+            float* row = zg + size_t(i) * size_t(a.dl);
+            if (kl + 1 < a.dl) {
+                if (aligned) {
+                    *reinterpret_cast<float2*>(row + kl) = z[p];
+                } else {
+                    row[kl] = z[p].x;
+                    row[kl + 1] = z[p].y;
+                }
+            } else if (kl < a.dl) {
+                row[kl] = z[p].x;
+            }
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) ticket = atomicAdd(a.tile_ticket + blockIdx.x, 1u);
+        __syncthreads();
+        if (ticket != gridDim.y - 1) return;  // not the last CTA of this tile
+        __threadfence();
+        if (threadIdx.x == 0) a.tile_ticket[blockIdx.x] = 0u;  // ready for the next launch
+    }
+    __syncthreads();
+    if (threadIdx.x < kTile) {
+        const int c = threadIdx.x;
+        const int64_t k = tile0 + c;
+        double ma = 0.0, scale = 1.0;
+        if (relax && (shared_path || k < a.dl)) {
+            const float* col = shared_path ? zs + c : zg + size_t(k);
+            const size_t ld = shared_path ? size_t(kTile) : size_t(a.dl);
+#pragma unroll 8
+            for (int j = 0; j < a.m; ++j) ma += double(col[size_t(j) * ld]);
+            ma *= 1.0 / a.m;
+            double va = 0.0;
+#pragma unroll 8
+            for (int j = 0; j < a.m; ++j) {
+                const double da = double(col[size_t(j) * ld]) - ma;
+                va += da * da;
+            }
+            const double sa = fmax(sqrt(va / (a.m - 1)), 1e-12);
+            scale = (1.0 - a.relax) + a.relax * fstat[c].y / sa;
+        }
+        rstat[c] = make_double2(ma, scale);
+    }
+    __syncthreads();
+    if (shared_path) {
+        const double2 s0 = rstat[2 * lane], s1 = rstat[2 * lane + 1];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int i = i0 + p;
+            if (i >= a.m) continue;
+            double* row = a.out64 + size_t(i) * size_t(a.dl);
+            const double vx = relax ? s0.x + s0.y * (double(z[p].x) - s0.x) : double(z[p].x);
+            const double vy = relax ? s1.x + s1.y * (double(z[p].y) - s1.x) : double(z[p].y);
+            if (kl + 1 < a.dl) {
+                if (aligned)
+                    *reinterpret_cast<double2*>(row + kl) = make_double2(vx, vy);
+                else {
+                    row[kl] = vx;
+                    row[kl + 1] = vy;
+                }
+            } else if (kl < a.dl) {
+                row[kl] = vx;
+            }
+        }
+        return;
+    }
+    // the last CTA writes the whole tile: member rows of 64 coordinates
+    for (int q = threadIdx.x; q < a.m * kTile; q += blockDim.x) {
+        const int j = q >> 6, c = q & (kTile - 1);
+        const int64_t k = tile0 + c;
+        if (k >= a.dl) continue;
+        const double v = double(zg[size_t(j) * size_t(a.dl) + size_t(k)]);
+        const double2 r = rstat[c];
+        a.out64[size_t(j) * size_t(a.dl) + size_t(k)] = relax ? r.x + r.y * (v - r.x) : v;
+    }
+}
+
 // kSorted: members of every coordinate are sorted once per analysis (the
 // componentwise score only needs the multiset of member values per
 // coordinate, proj/src/ensf.cpp:43-61), pass 1 becomes a binary search.
 // kPolyEvery: every kPolyEvery-th (member, particle) slot of the unrolled
 // member loop takes its two exponentials from ex2_poly2 instead of MUFU.
+// kFused: the whole analysis in one launch.  The prologue converts (and for
+// kSorted rank-sorts) the tile's fp64 forecast columns straight into shared
+// memory and takes the forecast statistics of relax_spread; the epilogue
+// runs relax_spread (proj/src/ensf.cpp:225-258) on the tile (in shared
+// memory, or - several CTAs per tile - by the tile's last CTA), so every
+// coordinate's statistics are the reference's member-order fp64 sums
+// (bit-identical to relax_kernel), and the fp64 analysis is written once.  No
+// prep_tiles / relax launches.
 template <int P, bool kMinibatch, bool kSorted, int kPolyEvery, int kMinBlocks = 1,
-          bool kGlobalX = false, int kThreads = 256, bool kShiftFree = true>
+          bool kGlobalX = false, int kThreads = 256, bool kShiftFree = true, bool kFused = false,
+          bool kNewtonRcp = true>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelArgs a, const float* __restrict__ xt,
                                                        const double2* __restrict__ ab,
                                                        const StepF32* __restrict__ steps,
@@ -179,6 +385,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
                                                        unsigned long long* __restrict__ status) {
     static_assert(!(kMinibatch && kSorted), "minibatches use the two-pass member loop");
     static_assert(!(kGlobalX && kSorted), "very large ensembles use the two-pass member loop");
+    static_assert(!(kFused && (kGlobalX || kMinibatch)), "fused: shared-memory tiles, no minibatch");
     constexpr int U = 4;  // member-loop unroll
     extern __shared__ float4 smem[];
     // the tile's members: shared memory, or (ensembles too large for it)
@@ -201,7 +408,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
     // coefficients are read from global memory (warp-uniform, L1-resident),
     // so any n_steps fits.
     __shared__ uint64_t tile_bar;
-    if (!kGlobalX) {
+    __shared__ double2 fstat[kTile];  // kFused: forecast (mean, sd) per coordinate
+    if (kFused) {
+        fused_prologue<kSorted>(a, reinterpret_cast<float*>(smem), tile0, fstat);
+    } else if (!kGlobalX) {
         if (threadIdx.x == 0) mbar_init(&tile_bar, 1);
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -229,18 +439,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
     // probes top, top/2, .., 1 reach pos <= 2 top - 1 >= J - 1; pos = J - 1
     // when all J members have u > 0 still yields the right pair (J-2, J-1)
     while (top * 2 < a.j_batch) top *= 2;
-    if (!kGlobalX) mbar_wait(&tile_bar, 0);  // the member tile has landed
+    if (!kGlobalX && !kFused) mbar_wait(&tile_bar, 0);  // the member tile has landed
 
     const int i0 = (blockIdx.y * nwarps + warp) * P;
     const uint64_t kg = uint64_t(a.k0 + kl);  // global coordinate of the pair's first entry
 
     float2 z[P];
-    int bad[P];
+    // first non-finite (particle, step) of this thread: min over (p << 30 | s)
+    // is the lowest particle and its first bad step (one register, not P)
+    uint32_t bad = UINT_MAX;
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-        z[p] = normal_pair_f32(kg, uint32_t(i0 + p), a.cycle_lo, a.rk);
-        bad[p] = INT_MAX;
-    }
+    for (int p = 0; p < P; ++p) z[p] = normal_pair_f32(kg, uint32_t(i0 + p), a.cycle_lo, a.rk);
 
     for (int s = 0; s < a.n_steps; ++s) {
         const StepF32 c = load_step(steps + s);
@@ -353,12 +562,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
         const uint64_t n0 = uint64_t(s + 1) * uint64_t(a.d_total) + kg;
 #pragma unroll
         for (int p = 0; p < P; ++p) {
-            // one MUFU.RCP for the pair: 1 / (den.x den.y).  Both sums lie in
-            // [2^-60, J] (the redo guarantees the lower bound), so the product
-            // is a normal float; a non-finite one only marks a diverged pair.
-            const float rr = rcp_approx(den[p].x * den[p].y);
-            const float2 q = __fmul2_rn(__fmul2_rn(num[p], make_float2(den[p].y, den[p].x)),
-                                        f2(rr));
+            // num / den per coordinate: a merged 1 / (den.x den.y) saves a
+            // MUFU op but couples the pair's roundings, and a window edge can
+            // split a pair, so results would depend on the sharding
+            const float2 q = recip_mul<kNewtonRcp>(num[p], den[p]);
             float2 lik;
             if (a.obs_atan) {
                 // h(z) = atan(z): H'^T R^-1 (y - h) = (B - A atan z) / (1 + z^2)
@@ -374,10 +581,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
             zn = __ffma2_rn(f2(c.sig), xi, zn);
             z[p] = zn;
             const bool fin = (fabsf(zn.x) <= FLT_MAX) && (fabsf(zn.y) <= FLT_MAX || !has_y);
-            if (!fin && bad[p] == INT_MAX) bad[p] = s;
+            if (!fin) bad = min(bad, (uint32_t(p) << 30) | uint32_t(s));
         }
     }
 
+    if (bad != UINT_MAX && kl < a.dl) {
+        const int i = i0 + int(bad >> 30);  // particles past m are padding
+        if (i < a.m) atomicMin(status, (uint64_t(i) << 32) | (bad & 0x3fffffffu));
+    }
+    if (kFused) {
+        fused_relax_epilogue<P>(a, reinterpret_cast<float*>(smem), z_out, tile0, kl, i0, fstat, z);
+        return;
+    }
 #pragma unroll
     for (int p = 0; p < P; ++p) {
         const int i = i0 + p;
@@ -393,8 +608,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
         } else if (kl < a.dl) {
             row[kl] = z[p].x;
         }
-        if (bad[p] != INT_MAX && kl < a.dl)
-            atomicMin(status, (uint64_t(i) << 32) | uint32_t(bad[p]));
     }
 }
 
@@ -719,13 +932,15 @@ int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
 // table in shared memory read their members from global memory (L1/L2).
 bool f32_members_global(int m) { return sizeof(float) * 64 * size_t(m) > 200 * 1024; }
 
-// Tuning knobs read once per process (experiments and the exact-shift
-// cross-check in tests/; the defaults are the measured best):
-//   TURBDA_F32_POLY=k         share of the exponentials taken by the FMA-pipe
-//                             polynomial: one (member, particle) slot in k of
-//                             the 16-slot unrolled member loop; 0 = all MUFU
+// Cross-check knobs read once per process (tests/ run both sides of each;
+// the defaults are the measured best, profiles/r02_sweeps.md):
+//   TURBDA_F32_POLY=0         every exponential on MUFU (default: the sorted
+//                             kernels take one (member, particle) slot in 8
+//                             from the FMA-pipe polynomial ex2_poly2)
 //   TURBDA_F32_EXACT_SHIFT=1  always take the reference's exact softmax
 //                             shift first (no shift-free pass)
+//   TURBDA_F32_UNFUSED=1      prep_tiles -> ensf_f32 -> relax as three launches
+//                             (the same arithmetic: bit-identical output)
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
     return e ? std::atoi(e) : dflt;
@@ -753,63 +968,97 @@ cudaError_t launch_kernel(K kern, dim3 grid, dim3 block, size_t smem, cudaStream
 //    with the same 1/8 share;
 //  * sorted, two or three tiles fit: 8-warp CTAs, 3 per SM, all MUFU;
 //  * unsorted tiles (N <= 24, configs 1 and 3: brute-force redo shift):
-//    CTAs of ceil(N/P) warps, 64 registers, kPolyUnsorted share;
+//    CTAs of ceil(N/P) warps, 64 registers, all MUFU (the 1/8, 3/16 and 1/4
+//    polynomial shares, 80-register and 32-48-register budgets, P = 1 / 2
+//    and Box-Muller on the FMA pipe all measured slower or equal at config
+//    3: the kernel sits at 86 % of the MUFU pipe, profiles/r02_sweeps.md);
+//  * all of these fused: one launch per analysis;
 //  * minibatches and ensembles whose tile exceeds shared memory: the
-//    two-pass member loop, all MUFU.
+//    two-pass member loop, all MUFU, unfused.
 constexpr int kPolySorted = 8;
 constexpr int kPolyUnsorted = 0;
 
 template <int P>
-cudaError_t launch_f32_p(const KernelArgs& a, const float* xt, const double2* ab,
+cudaError_t launch_f32_p(const KernelArgs& a, float* xt, const double2* ab,
                          const StepF32* steps, const int32_t* batches, float* z,
                          unsigned long long* status, cudaStream_t st, bool sorted) {
     static const int poly_env = env_int("TURBDA_F32_POLY", -1);
     static const bool exact = env_int("TURBDA_F32_EXACT_SHIFT", 0) != 0;
+    static const bool unfused = env_int("TURBDA_F32_UNFUSED", 0) != 0;
     const int groups = (a.m + P - 1) / P;
     const bool global_x = f32_members_global(a.m);
-    const size_t smem = global_x ? 0 : sizeof(float2) * 32 * size_t(a.m);
+    const size_t tile = sizeof(float) * kTile * size_t(a.m);
     const size_t smem_sm = size_t(227) * 1024;
-    const bool wide = sorted && !exact && smem * 2 > smem_sm;  // one tile per SM
+    const bool wide = sorted && !exact && tile * 2 > smem_sm;  // one tile per SM
     const int wmax = wide ? 32 : 8;
     const int nw = groups < wmax ? groups : wmax;
+    const unsigned ny = unsigned((groups + nw - 1) / nw);
+    const bool fused = !global_x && !a.minibatch && !exact && !unfused;
+    // fused: + the sort staging columns, and room for the epilogue's
+    // particles (nw P of them, which can exceed m by up to P - 1)
+    const size_t smem =
+        global_x ? 0
+        : !fused ? tile
+                 : std::max(tile + (sorted ? sizeof(float) * size_t(std::min(nw, kSortWarps)) *
+                                                 size_t(a.m)
+                                           : 0),
+                            sizeof(float) * kTile * size_t(nw) * size_t(P));
+    const unsigned tiles = unsigned((a.dl + kTile - 1) / kTile);
     const dim3 block(32 * nw);
-    const dim3 grid(unsigned((a.dl + kTile - 1) / kTile), unsigned((groups + nw - 1) / nw));
+    const dim3 grid(tiles, ny);
+    if (!fused) {
+        // fp64 forecast -> fp32 (sorted) tiles in global memory
+        if (sorted) {
+            if (tile > 48 * 1024) {
+                cudaError_t e = cudaFuncSetAttribute(prep_tiles_kernel<true>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     int(tile));
+                if (e != cudaSuccess) return e;
+            }
+            prep_tiles_kernel<true><<<tiles, 256, tile, st>>>(a.x64, a.m, a.dl, xt);
+        } else {
+            prep_tiles_kernel<false><<<tiles, 256, 0, st>>>(a.x64, a.m, a.dl, xt);
+        }
+        add_launches(1);
+        if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
+    }
     auto go = [&](auto kern) {
-        return launch_kernel(kern, grid, block, smem, st, a, xt, ab, steps, batches, z, status);
+        if (fused && ny > 1) {  // the last CTA of each tile resets its ticket
+            cudaError_t e = cudaMemsetAsync(a.tile_ticket, 0, sizeof(unsigned int) * tiles, st);
+            if (e != cudaSuccess) return e;
+        }
+        cudaError_t e = launch_kernel(kern, grid, block, smem, st, a, xt, ab, steps, batches, z,
+                                      status);
+        add_launches(1);
+        if (e != cudaSuccess || fused) return e;
+        relax_kernel<float><<<blocks_for(a.dl, 256), 256, 0, st>>>(z, a.x64, a.m, a.dl, a.relax,
+                                                                   a.out64);
+        add_launches(1);
+        return cudaGetLastError();
     };
     if (global_x)
         return a.minibatch ? go(ensf_f32_kernel<P, true, false, 0, 3, true>)
                            : go(ensf_f32_kernel<P, false, false, 0, 3, true>);
     if (a.minibatch) return go(ensf_f32_kernel<P, true, false, 0, 3>);
+    if (exact)
+        return sorted ? go(ensf_f32_kernel<P, false, true, 0, 3, false, 256, false>)
+                      : go(ensf_f32_kernel<P, false, false, 0, 4, false, 256, false>);
     if (!sorted) {
-        if (exact) return go(ensf_f32_kernel<P, false, false, 0, 4, false, 256, false>);
-        static const int minb = env_int("TURBDA_F32_MINB", 4);
-        if (minb == 3) {
-            switch (poly_env >= 0 ? poly_env : kPolyUnsorted) {
-                case 8: return go(ensf_f32_kernel<P, false, false, 8, 3>);
-                case 5: return go(ensf_f32_kernel<P, false, false, 5, 3>);
-                case 4: return go(ensf_f32_kernel<P, false, false, 4, 3>);
-                default: return go(ensf_f32_kernel<P, false, false, 0, 3>);
-            }
-        }
-        switch (poly_env >= 0 ? poly_env : kPolyUnsorted) {
-            case 8: return go(ensf_f32_kernel<P, false, false, 8, 4>);
-            case 5: return go(ensf_f32_kernel<P, false, false, 5, 4>);
-            case 4: return go(ensf_f32_kernel<P, false, false, 4, 4>);
-            default: return go(ensf_f32_kernel<P, false, false, 0, 4>);
-        }
+        return fused ? go(ensf_f32_kernel<P, false, false, kPolyUnsorted, 4, false, 256, true, true>)
+                     : go(ensf_f32_kernel<P, false, false, kPolyUnsorted, 4>);
     }
-    if (exact) return go(ensf_f32_kernel<P, false, true, 0, 3, false, 256, false>);
-    if (wide) return go(ensf_f32_kernel<P, false, true, kPolySorted, 1, false, 1024>);
+    if (wide)
+        return fused ? go(ensf_f32_kernel<P, false, true, kPolySorted, 1, false, 1024, true, true>)
+                     : go(ensf_f32_kernel<P, false, true, kPolySorted, 1, false, 1024>);
     if (smem * 4 <= smem_sm) {
-        switch (poly_env >= 0 ? poly_env : kPolySorted) {
-            case 5: return go(ensf_f32_kernel<P, false, true, 5, 4>);
-            case 4: return go(ensf_f32_kernel<P, false, true, 4, 4>);
-            case 0: return go(ensf_f32_kernel<P, false, true, 0, 4>);
-            default: return go(ensf_f32_kernel<P, false, true, 8, 4>);
-        }
+        if (poly_env == 0)
+            return fused ? go(ensf_f32_kernel<P, false, true, 0, 4, false, 256, true, true>)
+                         : go(ensf_f32_kernel<P, false, true, 0, 4>);
+        return fused ? go(ensf_f32_kernel<P, false, true, kPolySorted, 4, false, 256, true, true>)
+                     : go(ensf_f32_kernel<P, false, true, kPolySorted, 4>);
     }
-    return go(ensf_f32_kernel<P, false, true, 0, 3>);
+    return fused ? go(ensf_f32_kernel<P, false, true, 0, 3, false, 256, true, true>)
+                 : go(ensf_f32_kernel<P, false, true, 0, 3>);
 }
 
 template <int P, bool kSmemX>
@@ -885,34 +1134,19 @@ size_t ensf_f32_scratch_bytes(int m, int64_t dl) {
     return sizeof(float) * size_t(m) * size_t((dl + kTile - 1) / kTile) * kTile;
 }
 
-cudaError_t launch_ensf_f32(const KernelArgs& a, const double* x, const double2* ab,
-                            const StepF32* steps, const int32_t* batches, float* xt, float* z,
+cudaError_t launch_ensf_f32(const KernelArgs& a, const double2* ab, const StepF32* steps,
+                            const int32_t* batches, float* xt, float* z,
                             unsigned long long* status, cudaStream_t st, int64_t dl_concurrent) {
     if (a.dl <= 0) return cudaSuccess;
-    const unsigned tiles = unsigned((a.dl + kTile - 1) / kTile);
     // sorted tiles + binary-searched shift pay off past ~24 members; below,
     // the brute-force min pass is cheaper (measured, configs 1 and 3)
     const bool sorted = !a.minibatch && a.j_batch > 24 && !f32_members_global(a.m);
-    const size_t smem = sizeof(float) * size_t(a.m) * kTile;
-    if (sorted) {
-        if (smem > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(prep_tiles_kernel<true>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            if (e != cudaSuccess) return e;
-        }
-        prep_tiles_kernel<true><<<tiles, 256, smem, st>>>(x, a.m, a.dl, xt);
-    } else {
-        prep_tiles_kernel<false><<<tiles, 256, 0, st>>>(x, a.m, a.dl, xt);
-    }
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
     // particles per warp: 4 when the grid still fills the GPU (a full wave
     // is 148 SMs x 24 warps), fewer for small windows so more warps exist
     const int64_t tiles_n = (std::max(a.dl, dl_concurrent) + kTile - 1) / kTile;
     const auto warps_for = [&](int pp) { return tiles_n * ((a.m + pp - 1) / pp); };
     const int64_t wave = 148 * 24;
     // (particles past m in the last warp are computed and discarded)
-    static const int forced_p = env_int("TURBDA_F32_P", 0);  // experiments
     if ((a.m % 4 == 0 || a.m >= 32) && warps_for(4) >= wave)
         return launch_f32_p<4>(a, xt, ab, steps, batches, z, status, st, sorted);
     if ((a.m % 2 == 0 || a.m >= 16) && warps_for(2) >= wave / 2)

@@ -38,6 +38,7 @@
 #include <vector>
 
 #include <cub/cub.cuh>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <cufft.h>
 
@@ -234,6 +235,11 @@ struct PointArgs {
     double* vscratch;       // global V slots (kVGlobal)
     unsigned long long* singular;  // min point index with a singular transform
     int max_sweeps;
+    // Newton-Schulz points that did not converge are listed here and redone
+    // by the Jacobi kernel, which then walks only this list
+    int64_t* redo;                 // [P] point indices
+    unsigned int* redo_n;          // entries in `redo`
+    bool from_list;                // letkf_point_kernel: iterate redo[0 .. *redo_n)
 };
 
 template <bool kVGlobal>
@@ -268,7 +274,9 @@ __global__ void __launch_bounds__(256) letkf_point_kernel(PointArgs a) {
         blk[t] = (k1 << 16) | (k1 + r);
     }
 
-    for (int64_t pt = blockIdx.x; pt < a.P; pt += gridDim.x) {
+    const int64_t n_pts = a.from_list ? int64_t(*a.redo_n) : a.P;
+    for (int64_t it_pt = blockIdx.x; it_pt < n_pts; it_pt += gridDim.x) {
+        const int64_t pt = a.from_list ? a.redo[it_pt] : it_pt;
         const double count = a.fields[size_t(E + m) * a.P + pt];
         const int64_t row0 = pt, row1 = a.P + pt;
         if (!(count > 0.5)) {
@@ -620,7 +628,8 @@ __global__ void __launch_bounds__(256) letkf_point_ns_kernel(PointArgs a) {
         // iterate until ||Z Y - I||_max <= 1e-10 (the next update squares the
         // error below double rounding), at most 60 times; the final
         // iteration skips the Y update nobody reads
-        for (int it = 0; finite && it < 60; ++it) {
+        bool converged = false;
+        for (int it = 0; finite && it < a.max_sweeps; ++it) {
             // T = 3I - Z Y, with the residual max |T - 2I| = max |Z Y - I|
             g.compute(Z, Y, ld, lane);
             double res = g.store(T, ld, lane, -1.0, 3.0);
@@ -630,6 +639,7 @@ __global__ void __launch_bounds__(256) letkf_point_ns_kernel(PointArgs a) {
             res = 0.0;
             for (int w = 0; w < nt / 32; ++w) res = fmax(res, red[w]);
             const bool last = !(res > 1e-10);  // (fmax drops NaN: caught below)
+            converged = last;
             if (!last) {
                 // Y <- Y T / 2 (in place once every warp has read Y)
                 g.compute(Y, T, ld, lane);
@@ -652,6 +662,12 @@ __global__ void __launch_bounds__(256) letkf_point_ns_kernel(PointArgs a) {
         }
         if (__syncthreads_or(bad)) {
             if (tid == 0) atomicMin(a.singular, (unsigned long long)pt);
+            continue;
+        }
+        if (!converged) {
+            // still above the residual bound after 60 iterations (rounding-
+            // limited or stalled): the Jacobi eigensolver redoes this point
+            if (tid == 0) a.redo[atomicAdd(a.redo_n, 1u)] = pt;
             continue;
         }
         const double isc = rsqrt(cs);
@@ -737,7 +753,7 @@ struct LetkfWorkspace {
     cudaStream_t stream = nullptr;
     Buf x, y, r, idx, locs, out;
     Buf yb, dinn, rinv, cell, cell_sorted, order, sorted_obs, count, start, cub_tmp;
-    Buf fields, spec, vscratch, singular;
+    Buf fields, spec, vscratch, singular, redo;
     std::map<SpectrumKey, std::unique_ptr<Buf>> khat;
     int plan_nx = 0, plan_batch = 0;
     cufftHandle d2z = 0, z2d = 0;
@@ -957,8 +973,11 @@ int turbda_letkf_analyze(const turbda_letkf_params* p, const double* forecast, c
     LK_CUDA(w->sorted_obs.reserve(sizeof(uint32_t) * size_t(nb)));
     LK_CUDA(w->count.reserve(sizeof(int) * size_t(P + 1)));
     LK_CUDA(w->start.reserve(sizeof(int) * size_t(P + 1)));
-    LK_CUDA(w->singular.reserve(sizeof(unsigned long long)));
+    LK_CUDA(w->singular.reserve(sizeof(unsigned long long) + sizeof(unsigned int)));
     LK_CUDA(cudaMemsetAsync(w->singular.p, 0xff, sizeof(unsigned long long), s));
+    unsigned int* redo_n = reinterpret_cast<unsigned int*>(w->singular.as<unsigned char>() + 8);
+    LK_CUDA(cudaMemsetAsync(redo_n, 0, sizeof(unsigned int), s));
+    LK_CUDA(w->redo.reserve(sizeof(int64_t) * size_t(std::max<int64_t>(P, 1))));
     LK_CUDA(cudaMemsetAsync(w->count.p, 0, sizeof(int) * size_t(P + 1), s));
     if (nobs > 0) {
         letkf_obs_kernel<<<blocks_for(nobs, 256), 256, 0, s>>>(
@@ -1035,7 +1054,8 @@ int turbda_letkf_analyze(const turbda_letkf_params* p, const double* forecast, c
         int dev_smem = 0, nsm = 0;
         LK_CUDA(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         LK_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        if (m <= 64) {
+        const bool ns = m <= 64;
+        if (ns) {
             // tensor-core Newton-Schulz transform
             const int mp = (m + 7) & ~7;
             const size_t smem_ns = sizeof(double) * (3 * size_t(mp) * (mp + 4) + 4 * size_t(mp) + 8);
@@ -1049,6 +1069,15 @@ int turbda_letkf_analyze(const turbda_letkf_params* p, const double* forecast, c
             pn.x = dx;
             pn.out = dout;
             pn.singular = w->singular.as<unsigned long long>();
+            pn.redo = w->redo.as<int64_t>();
+            pn.redo_n = redo_n;
+            // iteration cap (60; TURBDA_LETKF_NS_ITERS lowers it in tests to
+            // force the Jacobi redo of unconverged points)
+            static const int ns_iters = [] {
+                const char* e = std::getenv("TURBDA_LETKF_NS_ITERS");
+                return e ? std::max(1, std::atoi(e)) : 60;
+            }();
+            pn.max_sweeps = ns_iters;
             void (*kern)(PointArgs) = nullptr;
             switch (mp / 8) {
                 case 1: kern = letkf_point_ns_kernel<1>; break;
@@ -1068,7 +1097,10 @@ int turbda_letkf_analyze(const turbda_letkf_params* p, const double* forecast, c
             kern<<<unsigned(grid_ns), 256, smem_ns, s>>>(pn);
             LK_CUDA(cudaGetLastError());
             add_launches(1);
-        } else {
+        }
+        // parallel cyclic Jacobi: every point for M > 64; otherwise only the
+        // points whose Newton-Schulz iteration did not converge (the kernel
+        // reads their count on the device and exits when there are none)
         const bool vglobal = 2 * mat + extra + 64 > size_t(dev_smem);
         const size_t smem = (vglobal ? mat : 2 * mat) + extra + 64;
         if (smem > size_t(dev_smem))
@@ -1084,6 +1116,9 @@ int turbda_letkf_analyze(const turbda_letkf_params* p, const double* forecast, c
         pa.out = dout;
         pa.singular = w->singular.as<unsigned long long>();
         pa.max_sweeps = 40;
+        pa.redo = w->redo.as<int64_t>();
+        pa.redo_n = redo_n;
+        pa.from_list = ns;
         int per_sm = 0;
         if (vglobal) {
             LK_CUDA(cudaFuncSetAttribute(letkf_point_kernel<true>,
@@ -1096,7 +1131,8 @@ int turbda_letkf_analyze(const turbda_letkf_params* p, const double* forecast, c
             LK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, letkf_point_kernel<false>,
                                                                   threads, smem));
         }
-        const int64_t grid = std::min<int64_t>(P, int64_t(std::max(per_sm, 1)) * nsm);
+        const int64_t grid = std::min<int64_t>(ns ? std::min<int64_t>(P, nsm) : P,
+                                               int64_t(std::max(per_sm, 1)) * nsm);
         if (vglobal) {
             LK_CUDA(w->vscratch.reserve(mat * size_t(grid)));
             pa.vscratch = w->vscratch.as<double>();
@@ -1106,7 +1142,6 @@ int turbda_letkf_analyze(const turbda_letkf_params* p, const double* forecast, c
         }
         LK_CUDA(cudaGetLastError());
         add_launches(1);
-        }
     }
     // 6. RTPS (alpha == 0 or a single member: the analysis is returned as is)
     if (p->rtps_alpha != 0.0 && m >= 2) {

@@ -186,13 +186,14 @@ def test_snapshot_checkpoint_of_device_ensemble(tb, tmp_path):
 # (proj/src/osse.cpp:182-253, unmodified, cuFFTW): 256 x 256 x 2, N = 64,
 # S = 100, every-4th-point observations, 20 cycles.
 CFG2_GOLDEN = ROOT / "tests" / "golden" / "cycle_cfg2_reference.json"
+CFG2_SHORT = ROOT / "tests" / "golden" / "cycle_cfg2_short_reference.json"
 REC_KEYS = ("time", "forecast_rmse", "analysis_rmse", "forecast_spread", "analysis_spread")
 
 
-def _cfg2_golden():
-    if not CFG2_GOLDEN.exists():
-        pytest.skip("tests/golden/cycle_cfg2_reference.json not generated")
-    return json.loads(CFG2_GOLDEN.read_text())
+def _cfg2_golden(path=CFG2_GOLDEN):
+    if not path.exists():
+        pytest.skip(f"{path.name} not generated")
+    return json.loads(path.read_text())
 
 
 def _csv(records):
@@ -203,8 +204,12 @@ def _csv(records):
 @pytest.mark.slow
 def test_cfg2_cycled_fp64_records_vs_reference(tb):
     """The faithful fp64 analysis inside the GPU-resident driver reproduces
-    every per-cycle record of the reference's own 20-cycle run to 1e-8."""
-    g = _cfg2_golden()
+    every per-cycle record of the reference's own 20-cycle run to 1e-8
+    (short spin-up: 240 h + 800 h of climatology keep the chaotic nature
+    run's amplification of the cuFFT rounding differences far below that;
+    after the 2400 h spin-up of the long fixture the truths themselves differ
+    at 1e-3, which is why that one is compared through its statistics)."""
+    g = _cfg2_golden(CFG2_SHORT)
     cfg = json.loads(json.dumps(g["config"]))
     cfg["ensf"]["precision"] = "fp64"
     got = tb.run_experiment(json.dumps(cfg))
@@ -213,7 +218,9 @@ def test_cfg2_cycled_fp64_records_vs_reference(tb):
     a = np.array([[r[k] for k in REC_KEYS] for r in got])
     b = np.array([[r[k] for k in REC_KEYS] for r in want])
     err = rel_l2(a, b)
-    print(f"config 2 cycled fp64 vs reference records: rel-L2 {err:.3e}")
+    per_cycle = [rel_l2(a[q], b[q]) for q in range(len(a))]
+    print(f"config 2 cycled fp64 vs reference records: rel-L2 {err:.3e}; per cycle "
+          + " ".join(f"{e:.1e}" for e in per_cycle))
     assert err <= 1e-8
 
 
@@ -236,3 +243,36 @@ def test_cfg2_cycled_fp32_rmse_within_2pct_and_bitwise_reruns(tb):
           f"(forecast {f_ref:.6f} / {f_gpu:.6f})")
     assert abs(m_gpu - m_ref) <= 0.02 * m_ref
     assert abs(f_gpu - f_ref) <= 0.02 * f_ref
+
+
+@pytest.mark.slow
+def test_cfg5_open_loop_cycles_vs_restatement(tb, port):
+    """BASELINE config 5 cycled (1024 x 1024 x 2, N = 128, arctan obs on every
+    4th point, 100 cycles) with the GPU-resident driver; at cycles 1, 10, 50
+    and 100 the probe returns the forecast and analysis ensembles over a
+    768-coordinate window and that cycle's observations, and the C
+    restatement (oracle/ensf_oracle.c, arctan likelihood: the extension has
+    no reference implementation) recomputes the window's analysis from the
+    same forecast with the same (seed, cycle) noise: open-loop per-cycle
+    parity at the fp32 tolerance."""
+    from paper_2407_12168_b200 import capi
+    from paper_2407_12168_b200.experiment import to_struct
+    n, m, stride = 1024, 128, 4
+    lx = 2 * np.pi * 10 * n / 64
+    cfg = {"grid": {"nx": n, "ny": n, "lx": lx, "ly": lx}, "cycles": 100, "ensemble_size": m,
+           "spinup_hours": 240.0, "clim_hours": 12.0 * (m + 4), "variant": "ensf",
+           "obs": {"thinning_stride": stride, "operator": "arctan"}, "ensf": {"n_steps": 100},
+           "seed": 7}
+    d = 2 * n * n
+    k0, w = 1_500_004, 768
+    idx_all = np.arange(0, d, stride, dtype=np.int64)
+    e = to_struct(cfg)
+    rec, probes = capi.run_experiment_probe(e, [1, 10, 50, 100], k0, w, idx_all.size)
+    assert len(rec) == 100 and np.isfinite(rec).all()
+    sel = (idx_all >= k0) & (idx_all < k0 + w)
+    for k, (fc, an, y) in sorted(probes.items()):
+        want = port.analyze(fc, y[sel], e.obs_r, idx_all[sel], n_steps=100, seed=7, cycle=k,
+                            k0=k0, d_total=d, arctan=True)
+        err = rel_l2(an, want)
+        print(f"config 5 cycle {k}: window analysis vs restatement rel-L2 {err:.2e}")
+        assert err <= 1e-4, (k, err)

@@ -132,3 +132,27 @@ def test_long_step_table(capi, port, precision, tol):
 def test_empty_window_without_communicator_is_a_no_op(capi):
     p = capi.params(d_total=4096, k0=4096, d_local=0, obs_dim=0, n_members=8, device=0)
     capi.analyze(p, np.zeros((8, 0)), np.zeros(0), np.zeros(0), None, np.zeros((8, 0)))
+
+
+def test_pageable_staging_ring_matches_pinned_and_rows(capi):
+    """Pageable host arrays above 32 MB go through the pinned staging ring
+    (pool-threaded gather / scatter, DMA from pinned slots); pinned arrays and
+    per-member row pointers (turbda_ensf_analyze_rows, the C++ Ensemble
+    layout) give the same bits."""
+    import ctypes as C
+    import torch
+    m, d = 64, 80_000 + 37  # 41 MB of forecast, ragged chunks
+    g = np.random.default_rng(23)
+    x = g.standard_normal((m, d))
+    y = g.standard_normal(d)
+    page = capi.analyze_host(x, y, 1.0, None, n_steps=20)
+    px = torch.from_numpy(x).pin_memory().numpy()
+    pinned = capi.analyze_host(px, y, 1.0, None, n_steps=20)
+    assert np.array_equal(page, pinned)
+    rows = [np.array(x[j]) for j in range(m)]
+    orows = [np.empty(d) for _ in range(m)]
+    rp = (C.c_void_p * m)(*[r.ctypes.data for r in rows])
+    op = (C.c_void_p * m)(*[o.ctypes.data for o in orows])
+    p = capi.params(d_total=d, d_local=d, obs_dim=d, n_members=m, n_steps=20, device=0)
+    capi.analyze_rows(p, rp, y, np.ones(d), None, op)
+    assert np.array_equal(np.stack(orows), page)

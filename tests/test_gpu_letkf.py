@@ -197,3 +197,27 @@ def test_letkf_ill_conditioned_local_problems(capi, r, tol):
     got = capi.letkf_analyze(x, y, r, nx=n, ny=n, cutoff_km=1500.0)
     want = L.letkf_analyze(x, y, r, None, n, n, cutoff_km=1500.0)
     assert rel_err(got, want) < tol
+
+
+def test_unconverged_newton_schulz_points_redone_by_jacobi(tmp_path):
+    """With the Newton-Schulz iteration capped at 3 (TURBDA_LETKF_NS_ITERS, a
+    fresh process) no point converges: every one is listed and redone by the
+    Jacobi eigensolver, and the analysis still matches the restatement."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    n, m = 16, 20
+    d = 2 * n * n
+    x = ens(m, d, 44)
+    y = np.random.default_rng(9).standard_normal(d)
+    np.save(tmp_path / "x.npy", x)
+    np.save(tmp_path / "y.npy", y)
+    code = ("import numpy as np, sys; from paper_2407_12168_b200 import capi; d = sys.argv[1]; "
+            "x = np.load(d + '/x.npy'); y = np.load(d + '/y.npy'); "
+            f"np.save(d + '/out.npy', capi.letkf_analyze(x, y, 0.5, None, nx={n}, ny={n}))")
+    env = dict(os.environ, TURBDA_LETKF_NS_ITERS="3")
+    subprocess.run([sys.executable, "-c", code, str(tmp_path)], check=True, env=env, cwd=str(ROOT))
+    got = np.load(tmp_path / "out.npy")
+    want = L.letkf_analyze(x, y, 0.5, None, n, n)
+    assert rel_err(got, want) < TOL

@@ -353,8 +353,10 @@ def test_cfg4_cfg5_full_size_window_vs_port(capi, port, d, m, stride, arctan, k0
 def test_wide_cta_one_tile_per_sm_vs_port(capi, port, m):
     """Ensembles whose member tile leaves room for one CTA per SM (N >= ~440)
     run 32-warp CTAs with the polynomial share (config 4's path); ragged
-    particle groups (N = 450) and a ragged last tile (d = 130)."""
-    x, y, idx, _ = conditioned_inputs(m, 130, stride=3)
+    particle groups (N = 450) and a ragged last tile (d = 2050: 33 tiles, so
+    tiles x ceil(N/4) fills a wave and P = 4 is chosen, which is the
+    particles-per-warp count whose 16-slot loop holds the polynomial slots)."""
+    x, y, idx, _ = conditioned_inputs(m, 2050, stride=3)
     x = x.astype(np.float32).astype(np.float64)
     y = y.astype(np.float32).astype(np.float64)
     want = port.analyze(x, y, 0.5, idx, n_steps=20)
@@ -490,3 +492,31 @@ def test_async_calls_on_two_streams_do_not_share_scratch(capi):
     torch.cuda.synchronize()
     for (out, *_), want in zip(outs, wants):
         assert np.array_equal(out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("m,d,stride", [(64, 4096 + 6, 4), (20, 4096, 1), (128, 2048, 3),
+                                        (512, 640, 1), (200, 4700, 2)])
+def test_fused_kernel_bit_identical_to_three_launches(capi, tmp_path, m, d, stride):
+    """The fused analysis (tile conversion/sort prologue, relax_spread epilogue
+    over a cluster of the tile's CTAs through distributed shared memory) vs
+    prep_tiles -> ensf_f32 -> relax_kernel (TURBDA_F32_UNFUSED=1, a fresh
+    process): bit-identical, for cluster sizes 1 (N = 20), 2-8 and the
+    32-warp one-tile-per-SM CTAs (N = 512)."""
+    import os
+    import subprocess
+    import sys
+    x, y, idx, _ = conditioned_inputs(m, d, stride=stride)
+    np.save(tmp_path / "x.npy", x)
+    np.save(tmp_path / "y.npy", y)
+    np.save(tmp_path / "i.npy", idx if idx is not None else np.zeros(0, np.int64))
+    code = ("import numpy as np, sys; from paper_2407_12168_b200 import capi; "
+            "d = sys.argv[1]; x, y, i = (np.load(d + f) for f in ('/x.npy', '/y.npy', '/i.npy')); "
+            "i = i if i.size else None; "
+            "np.save(d + '/out.npy', capi.analyze_host(x, y, 0.7, i, n_steps=30, relax_factor=0.6))")
+    env = dict(os.environ, TURBDA_F32_UNFUSED="1")
+    subprocess.run([sys.executable, "-c", code, str(tmp_path)], check=True, env=env,
+                   cwd=str(Path(__file__).resolve().parents[1]))
+    three = np.load(tmp_path / "out.npy")
+    fused = capi.analyze_host(x, y, 0.7, idx, n_steps=30, relax_factor=0.6)
+    assert np.isfinite(fused).all()
+    assert np.array_equal(fused, three)

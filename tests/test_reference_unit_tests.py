@@ -99,3 +99,24 @@ def test_cpp_letkf_api_on_b200():
     r = _run_cpp_letkf()
     print(r.stdout[-3000:])
     assert r.returncode == 0 and "failed=0" in r.stdout, r.stdout
+
+
+REF_LETKF_BIN = ROOT / "oracle" / "_ref" / "reftests_ref_letkf"
+
+
+def test_reference_letkf_tests_pin_the_eigen_subset():
+    """proj/tests/test_letkf.cpp against the reference's own letkf.cpp, both
+    compiled over oracle/ref_shadow/Eigen/Dense (Eigen is absent here): every
+    host-only case passes, which pins the Eigen subset - and with it the LETKF
+    oracle the GPU arm is compared with - on the reference's closed forms
+    (scalar Kalman update, ETKF identities, global-ETKF limit, RTPS)."""
+    passed, failed, out = _run(binary=REF_LETKF_BIN)
+    host_only = failed - {"letkf pulls a climatological ensemble toward the truth"}
+    assert len(passed) >= 13 and not host_only, out
+
+
+@pytest.mark.gpu
+def test_reference_letkf_tests_all_pass_on_gpu_box():
+    """The one case that needs the SQG nature run (cuFFTW) passes too."""
+    passed, failed, out = _run(binary=REF_LETKF_BIN)
+    assert len(passed) == 14 and not failed, out
