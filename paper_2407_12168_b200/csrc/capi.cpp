@@ -75,8 +75,10 @@ int cuda_fail(turbda_status* st, cudaError_t e, const char* where) {
 class CopyPool {
 public:
     static CopyPool& get() {
-        static CopyPool pool;
-        return pool;
+        // never destroyed: the detached workers wait on cv_ until the process
+        // ends, and destroying a condition variable with waiters blocks exit
+        static CopyPool* pool = new CopyPool;
+        return *pool;
     }
     // fn(t) for t in [0, n), spread over the pool; returns when all are done
     void run(int64_t n, const std::function<void(int64_t)>& fn) {

@@ -993,7 +993,13 @@ cudaError_t launch_f32_p(const KernelArgs& a, float* xt, const double2* ab,
     const int wmax = wide ? 32 : 8;
     const int nw = groups < wmax ? groups : wmax;
     const unsigned ny = unsigned((groups + nw - 1) / nw);
-    const bool fused = !global_x && !a.minibatch && !exact && !unfused;
+    // fused when a tile spans at most 3 CTAs: measured faster there (config
+    // 3: 1 CTA, 190.3 -> 188.0 ms; config 1: 3 CTAs, 0.109 -> 0.104 ms;
+    // config 2: 2 CTAs, equal) and slower at 4 (config 5: 744 -> 756 ms,
+    // config 4: 5588 -> 5922 ms), where the per-CTA prologue (fp64 loads,
+    // the tile sort) repeated by every CTA of the tile and the last CTA's
+    // relax of N x 64 values outweigh the two launches saved
+    const bool fused = !global_x && !a.minibatch && !exact && !unfused && ny <= 3;
     // fused: + the sort staging columns, and room for the epilogue's
     // particles (nw P of them, which can exceed m by up to P - 1)
     const size_t smem =

@@ -24,6 +24,8 @@
 #include <cstdlib>
 #include <climits>
 #include <cstdint>
+#include <mutex>
+#include <vector>
 
 #include "ensf_device.h"
 #include "philox.cuh"
@@ -698,6 +700,46 @@ cudaError_t launch_joint_gram(const KernelArgs& a, const JointPlan& pl, const do
     return cudaGetLastError();
 }
 
+// Per-step launch helpers: the dynamic shared-memory opt-in and the
+// occupancy-derived grid of the persistent apply kernels are resolved once
+// per (device, kernel, size) instead of with four runtime queries every
+// pseudo-step (the joint mode launches ~5 kernels per step).
+struct LaunchShape {
+    int device;
+    const void* kern;
+    size_t smem;
+    int threads;
+    int64_t max_ctas;  // resident CTAs on the whole device
+};
+std::mutex g_shape_mu;
+std::vector<LaunchShape> g_shapes;
+
+template <class K>
+cudaError_t resident_ctas(K kern, int threads, size_t smem, int64_t* out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_shape_mu);
+    for (const LaunchShape& q : g_shapes)
+        if (q.device == dev && q.kern == reinterpret_cast<const void*>(kern) && q.smem == smem &&
+            q.threads == threads) {
+            *out = q.max_ctas;
+            return cudaSuccess;
+        }
+    if (smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+    }
+    int nsm = 0, ps = 0;
+    e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, threads, smem);
+    if (e != cudaSuccess) return e;
+    *out = int64_t(std::max(ps, 1)) * nsm;
+    g_shapes.push_back({dev, reinterpret_cast<const void*>(kern), smem, threads, *out});
+    return cudaSuccess;
+}
+
 cudaError_t launch_joint_update(const KernelArgs& a, const double* x, const double2* ab,
                                 const double* red, double* wn, const StepF64& c, int step,
                                 double* z, unsigned long long* status, bool f32_noise,
@@ -715,18 +757,11 @@ cudaError_t launch_joint_update(const KernelArgs& a, const double* x, const doub
         const size_t smem = sizeof(double) * (size_t(mp8) * (mk + 4) + 2 * size_t(mk) * kTcLdx + 256);
         const int threads = 32 * (mp8 / 8);
         auto kern = f32_noise ? joint_apply_tc_kernel<true> : joint_apply_tc_kernel<false>;
-        int ps = 0;
-        if (smem > 48 * 1024) {
-            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            if (e != cudaSuccess) return e;
-        }
-        int dev = 0, nsm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, threads, smem);
+        int64_t resident = 0;
+        e = resident_ctas(kern, threads, smem, &resident);
         if (e != cudaSuccess) return e;
         const int64_t ntiles = (a.dl + 63) / 64;
-        const int64_t grid = std::min<int64_t>(ntiles, int64_t(std::max(ps, 1)) * nsm);
+        const int64_t grid = std::min<int64_t>(ntiles, resident);
         kern<<<unsigned(grid), threads, smem, st>>>(a, x, ab, wn, c, step, z, status, ntiles);
         return cudaGetLastError();
     }
@@ -734,18 +769,12 @@ cudaError_t launch_joint_update(const KernelArgs& a, const double* x, const doub
         const size_t smem = sizeof(double) * (2 * size_t(64) * kBigLdw + 2 * size_t(kBigK) * kTcLdx) +
                             sizeof(double2) * 64;
         auto kern = f32_noise ? joint_apply_tc_big_kernel<true> : joint_apply_tc_big_kernel<false>;
-        if (smem > 48 * 1024) {
-            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            if (e != cudaSuccess) return e;
-        }
-        int dev = 0, nsm = 0, ps = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, 256, smem);
+        int64_t resident = 0;
+        e = resident_ctas(kern, 256, smem, &resident);
         if (e != cudaSuccess) return e;
         const int64_t ntiles = (a.dl + 63) / 64;
         const int64_t items = ntiles * ((a.m + 63) / 64);
-        const int64_t grid = std::min<int64_t>(items, int64_t(std::max(ps, 1)) * nsm);
+        const int64_t grid = std::min<int64_t>(items, resident);
         kern<<<unsigned(grid), 256, smem, st>>>(a, x, ab, wn, c, step, z, status, ntiles);
         return cudaGetLastError();
     }

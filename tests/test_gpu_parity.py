@@ -494,14 +494,16 @@ def test_async_calls_on_two_streams_do_not_share_scratch(capi):
         assert np.array_equal(out.cpu().numpy(), want)
 
 
-@pytest.mark.parametrize("m,d,stride", [(64, 4096 + 6, 4), (20, 4096, 1), (128, 2048, 3),
-                                        (512, 640, 1), (200, 4700, 2)])
+@pytest.mark.parametrize("m,d,stride", [(20, 46000, 1), (64, 14406, 4), (30, 30000, 1),
+                                        (96, 9600, 3), (20, 4096, 1), (24, 3000, 3)])
 def test_fused_kernel_bit_identical_to_three_launches(capi, tmp_path, m, d, stride):
     """The fused analysis (tile conversion/sort prologue, relax_spread epilogue
-    over a cluster of the tile's CTAs through distributed shared memory) vs
-    prep_tiles -> ensf_f32 -> relax_kernel (TURBDA_F32_UNFUSED=1, a fresh
-    process): bit-identical, for cluster sizes 1 (N = 20), 2-8 and the
-    32-warp one-tile-per-SM CTAs (N = 512)."""
+    in shared memory for one CTA per tile, by the tile's last CTA through the
+    global scratch for 2-3) vs prep_tiles -> ensf_f32 -> relax_kernel
+    (TURBDA_F32_UNFUSED=1, a fresh process): bit-identical.  Cases: one CTA
+    per tile (N = 20, P = 4, config 3's shape), sorted tiles over 2 CTAs
+    (N = 64, P = 4; N = 30, P = 2) and 3 CTAs (N = 96), unsorted over 3
+    (N = 20 and 24, P = 1), ragged last tiles."""
     import os
     import subprocess
     import sys
