@@ -269,14 +269,16 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def spawn_ranks(n):
+def spawn_ranks(n, json_out):
     """--gpus N without a launcher: one process per GPU under
-    torch.distributed.run (the driver's own launch line), stdout passed up."""
+    torch.distributed.run (the driver's own launch line); the ranks write to
+    the original stdout (rank 0's JSON line), everything else to stderr."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            str(Path(__file__).resolve())] + sys.argv[1:]
     print(f"bench: spawning {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
-    return subprocess.call(cmd)
+    json_out.flush()
+    return subprocess.call(cmd, stdout=json_out)
 
 
 def timed_analyses(torch, fn, n, stream):
@@ -319,7 +321,7 @@ def main():
         run_reference_arm(args, json_out)
         return
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
-        sys.exit(spawn_ranks(args.gpus))
+        sys.exit(spawn_ranks(args.gpus, json_out))
 
     import torch
     import torch.distributed as dist
@@ -365,6 +367,9 @@ def main():
     obs_dim = dsets[0][1].numel()
 
     def mkparams(precision, flags, cycle=1):
+        # the joint mode's windows share their per-step distances over the
+        # library communicator: TURBDA_SHARDED on every rank
+        flags |= capi.SHARDED if (joint and world > 1) else 0
         return capi.params(d_total=d_total, k0=k0, d_local=d, obs_dim=obs_dim, n_members=m,
                            n_steps=s, obs_kind=obs_kind, precision=precision, device=local,
                            flags=flags, cycle=cycle,

@@ -85,10 +85,15 @@ typedef enum turbda_precision {
                                      /* the Python binding, bindings/python/      */
                                      /* core.cpp); host or device pointer as the  */
                                      /* other arrays                              */
-#define TURBDA_SHARDED 0x8u          /* turbda_diag: `members` / `truth` are this */
-                                     /* rank's shard of a state split over the    */
-                                     /* ranks of turbda_comm_init; the partial    */
-                                     /* sums are allreduced over them             */
+#define TURBDA_SHARDED 0x8u          /* the call is this rank's window / shard of  */
+                                     /* a state split over the ranks of           */
+                                     /* turbda_comm_init, and every rank makes    */
+                                     /* the same call: the analysis min-reduces   */
+                                     /* its divergence verdict (the joint mode    */
+                                     /* also allreduces its per-step distances),  */
+                                     /* turbda_diag its partial sums.  Without    */
+                                     /* it a call is local even when a            */
+                                     /* communicator exists                       */
 
 typedef struct turbda_status {
     int32_t code;              /* turbda_code                                   */
@@ -202,13 +207,13 @@ TURBDA_API int turbda_diag(const double* members, int32_t n_members, int64_t d, 
 
 /*
  * NCCL communicator for state-dimension sharding across processes (one rank
- * per GPU).  The joint score mode exchanges the per-step distances through
- * it; the componentwise mode needs none, but with a communicator a window
- * (d_local < d_total) min-reduces its divergence verdict, so every rank
- * reports the unsharded run's SamplerDivergedError, and turbda_diag with
- * TURBDA_SHARDED sums its partials over the ranks.  A rank whose window is
- * empty (d_local == 0) still joins every collective of the call, so its
- * peers never wait on it.  NCCL is loaded on first use
+ * per GPU).  Calls flagged TURBDA_SHARDED use it: the joint score mode
+ * exchanges the per-step distances through it; the componentwise mode needs
+ * none, but a sharded window min-reduces its divergence verdict, so every
+ * rank reports the unsharded run's SamplerDivergedError, and turbda_diag
+ * sums its partials over the ranks.  A rank whose window is empty
+ * (d_local == 0) still joins every collective of the call, so its peers
+ * never wait on it.  NCCL is loaded on first use
  * (dlopen("libnccl.so.2"), the copy torch already loaded when present).
  *   rank 0: turbda_comm_unique_id(id) -> broadcast the 128 bytes -> every
  *   rank: turbda_comm_init(device, rank, world, id).

@@ -227,10 +227,12 @@ def check(device: int, p: EnsfParams) -> Status:
 def analyze_host(members, y, r=1.0, idx=None, *, n_steps=100, eps=0.01, minibatch_j=0,
                  damping_t=1.0, relax_factor=1.0, seed=7, cycle=1, precision=FP32, device=-1,
                  device_count=1, k0=0, d_total=None, arctan=False, joint=False,
-                 r_uniform=False):
+                 r_uniform=False, sharded=False):
     """numpy-in / numpy-out analysis over the window [k0, k0 + d) of a state
     of dimension d_total (defaults to the whole state).  ``r_uniform``: pass
-    the scalar ``r`` once (TURBDA_R_UNIFORM) instead of an obs_dim copy."""
+    the scalar ``r`` once (TURBDA_R_UNIFORM) instead of an obs_dim copy.
+    ``sharded``: this rank's window of a state split over the device's
+    communicator (TURBDA_SHARDED; every rank makes the same call)."""
     x = np.ascontiguousarray(members, dtype=np.float64)
     m, d = x.shape
     y = np.ascontiguousarray(y, dtype=np.float64)
@@ -246,7 +248,7 @@ def analyze_host(members, y, r=1.0, idx=None, *, n_steps=100, eps=0.01, minibatc
                relax_factor=relax_factor, seed=seed, cycle=cycle, precision=precision,
                device=device, device_count=device_count,
                score_mode=SCORE_JOINT if joint else SCORE_COMPONENTWISE,
-               flags=R_UNIFORM if r_uniform else 0)
+               flags=(R_UNIFORM if r_uniform else 0) | (SHARDED if sharded else 0))
     out = np.empty_like(x)
     analyze(p, x, y, r, ix, out)
     return out

@@ -813,7 +813,7 @@ int nccl_fail(turbda_status* st, NcclApi* api, ncclResult_t r, const char* where
 // unsharded reference run raises.
 int reduce_verdict_across_ranks(const turbda_ensf_params* p, Workspace* w,
                                 unsigned long long* dstatus, cudaStream_t s, turbda_status* st) {
-    if (!w->comm || w->comm_world <= 1 || p->d_local >= p->d_total) return TURBDA_OK;
+    if (!(p->flags & TURBDA_SHARDED) || !w->comm || w->comm_world <= 1) return TURBDA_OK;
     NcclApi* api = nccl_api();
     if (!api) return fail(st, TURBDA_CUDA, "libnccl.so.2 not loadable");
     const ncclResult_t r = api->all_reduce(dstatus, dstatus, 1, ncclUint64, ncclMin,
@@ -998,7 +998,7 @@ int join_empty_window(const turbda_ensf_params* p, int device, cudaStream_t user
     TB_CUDA(cudaSetDevice(device));
     Workspace* w = workspace(device);
     std::lock_guard<std::mutex> lk(w->mu);
-    if (!w->comm || w->comm_world <= 1 || p->d_total == 0) return TURBDA_OK;
+    if (!(p->flags & TURBDA_SHARDED) || !w->comm || w->comm_world <= 1) return TURBDA_OK;
     if (int rc = ws_init(w, st)) return rc;
     const bool on_dev = (p->flags & TURBDA_INPUTS_ON_DEVICE) != 0;
     cudaStream_t s = user_stream ? user_stream : (on_dev ? cudaStreamLegacy : w->stream);
@@ -1100,10 +1100,13 @@ int analyze_impl(const turbda_ensf_params* p, const double* forecast, const doub
             // a window of a larger state shares the distances through the
             // device's communicator (turbda_comm_init)
             Workspace* w = workspace(dev0);
-            void* comm = (p->d_local < p->d_total && w->comm_world > 1) ? w->comm : nullptr;
+            const bool sharded = (p->flags & TURBDA_SHARDED) != 0;
+            void* comm = (sharded && w->comm_world > 1) ? w->comm : nullptr;
+            if (sharded && !comm)
+                return fail(st, TURBDA_CONFIG, "TURBDA_SHARDED needs turbda_comm_init on this device");
             if (p->d_local < p->d_total && !comm)
                 return fail(st, TURBDA_CONFIG,
-                            "joint score mode on a window needs turbda_comm_init on this device");
+                            "joint score mode on a window needs TURBDA_SHARDED and turbda_comm_init");
             return run_joint(p, Window{0, p->d_local}, dev0, forecast, frows, y, r_diag, obs_idx,
                              analysis_out, orows, static_cast<cudaStream_t>(stream), comm, st);
         }

@@ -8,7 +8,28 @@
 
 #include "philox_keys.h"
 
+// Checked builds (make CHECKED=1): device-side bounds assertions on every
+// shared-memory tile / staging / scratch index and the global rows the
+// kernels write - the stand-in for compute-sanitizer, which is closed on the
+// GPU pool (profiles/r02_compute_sanitizer_closed.txt).  A failed check
+// traps, so the call returns TURBDA_CUDA (cudaErrorAssert).
+#ifdef TURBDA_CHECKED
+#include <cassert>
+#define TB_CHECK(cond) assert(cond)
+#else
+#define TB_CHECK(cond) ((void)0)
+#endif
+
 namespace tb200 {
+
+#ifdef __CUDACC__
+// bytes of dynamic shared memory of the running launch
+__device__ __forceinline__ uint32_t dyn_smem_bytes() {
+    uint32_t r;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+    return r;
+}
+#endif
 
 // Per pseudo-time step coefficients of the fp32 fast kernel (32 B).  All are
 // derived on the host in fp64 from the reference's time grid

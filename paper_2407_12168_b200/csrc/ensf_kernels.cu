@@ -204,6 +204,7 @@ __device__ __forceinline__ void fused_prologue(const KernelArgs& a, float* tile,
         } else if (k < a.dl) {
             v.x = __ldg(src);
         }
+        TB_CHECK(sizeof(float) * size_t(j * kTile + c + 2) <= dyn_smem_bytes());
         *reinterpret_cast<float2*>(tile + j * kTile + c) = make_float2(float(v.x), float(v.y));
     }
     if (threadIdx.x < kTile) {
@@ -233,6 +234,8 @@ __device__ __forceinline__ void fused_prologue(const KernelArgs& a, float* tile,
     float* stage = tile + size_t(m) * kTile + size_t(warp) * size_t(m);  // [m] per warp
     if (warp < sorters) {
         for (int c = warp; c < kTile; c += sorters) {
+            TB_CHECK(sizeof(float) * (size_t(m) * kTile + size_t(warp + 1) * size_t(m)) <=
+                     dyn_smem_bytes());
             for (int j = lane; j < m; j += 32) stage[j] = tile[j * kTile + c];
             __syncwarp();
             for (int j = lane; j < m; j += 32) {
@@ -243,6 +246,7 @@ __device__ __forceinline__ void fused_prologue(const KernelArgs& a, float* tile,
                     const float ki = sort_key(stage[i]);
                     rank += (ki < kv) || (ki == kv && i < j);
                 }
+                TB_CHECK(rank < m);
                 tile[rank * kTile + c] = v;
             }
             __syncwarp();
@@ -277,6 +281,7 @@ __device__ __forceinline__ void fused_relax_epilogue(const KernelArgs& a, float*
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             const int il = warp * P + p;
+            TB_CHECK(sizeof(float) * size_t(il * kTile + 2 * lane + 2) <= dyn_smem_bytes());
             zs[il * kTile + 2 * lane] = z[p].x;
             zs[il * kTile + 2 * lane + 1] = z[p].y;
         }
@@ -299,7 +304,9 @@ __device__ __forceinline__ void fused_relax_epilogue(const KernelArgs& a, float*
         }
         __threadfence();
         __syncthreads();
+        TB_CHECK(a.tile_ticket != nullptr);
         if (threadIdx.x == 0) ticket = atomicAdd(a.tile_ticket + blockIdx.x, 1u);
+        TB_CHECK(ticket < gridDim.y);
         __syncthreads();
         if (ticket != gridDim.y - 1) return;  // not the last CTA of this tile
         __threadfence();
@@ -475,6 +482,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
 #pragma unroll
                 for (int uu = 0; uu < U; ++uu) {
                     const int j = kMinibatch ? __ldg(bt + jj + uu) : jj + uu;
+                    TB_CHECK(j >= 0 && j < a.m);
+                    TB_CHECK(kGlobalX || sizeof(float2) * size_t(j * 32 + lane + 1) <= dyn_smem_bytes());
                     const float2 xv = kGlobalX ? __ldg(xs + j * 32 + lane) : xs[j * 32 + lane];
 #pragma unroll
                     for (int p = 0; p < P; ++p) {
@@ -853,6 +862,7 @@ __global__ void obs_select_runs_kernel(const double* __restrict__ y, const doubl
     if (t >= obs_dim) return;
     const int64_t key = keys[t];
     if (t > 0 && keys[t - 1] == key) return;
+    TB_CHECK(pos[t] >= 0 && pos[t] < obs_dim);
     const int64_t k = key - k0;
     if (k < 0 || k >= dl) return;
     double A = 0.0, B = 0.0;

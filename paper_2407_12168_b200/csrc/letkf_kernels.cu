@@ -667,7 +667,11 @@ __global__ void __launch_bounds__(256) letkf_point_ns_kernel(PointArgs a) {
         if (!converged) {
             // still above the residual bound after 60 iterations (rounding-
             // limited or stalled): the Jacobi eigensolver redoes this point
-            if (tid == 0) a.redo[atomicAdd(a.redo_n, 1u)] = pt;
+            if (tid == 0) {
+                const unsigned slot = atomicAdd(a.redo_n, 1u);
+                TB_CHECK(int64_t(slot) < a.P);
+                a.redo[slot] = pt;
+            }
             continue;
         }
         const double isc = rsqrt(cs);

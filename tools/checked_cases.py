@@ -1,4 +1,4 @@
-"""Small analyses, one kernel family each, for compute-sanitizer (tools/sanitize.sh)."""
+"""Small analyses, one kernel family each, for the bounds-checked build (tools/checked_run.sh)."""
 import os
 import sys
 from pathlib import Path
@@ -18,7 +18,7 @@ def main(case):
         y = g.standard_normal(2 * n * n)
         capi.letkf_analyze(x, y, 0.5, None, nx=n, ny=n)
         return
-    m = {"f32_sorted_cluster": 64, "f32_unsorted": 20, "f32_minibatch": 32, "f32_exact_tma": 64,
+    m = {"f32_sorted_multi_cta": 64, "f32_unsorted": 20, "f32_minibatch": 32, "f32_exact_tma": 64,
          "f64": 20, "joint": 16}[case]
     d = 256 + 6  # ragged last tile
     x, y, idx, _ = conditioned_inputs(m, d, stride=3)

@@ -40,7 +40,7 @@ def main():
     x = 0.05 * x
     lo, hi = d * rank // world, d * (rank + 1) // world
     part_j = capi.analyze_host(x[:, lo:hi], y[lo:hi], 4.0, None, n_steps=20, joint=True,
-                               device=local, k0=lo, d_total=d, precision=capi.FP64)
+                               device=local, k0=lo, d_total=d, precision=capi.FP64, sharded=True)
     part_c = capi.analyze_host(x[:, lo:hi], y[lo:hi], 4.0, None, n_steps=20, device=local,
                                k0=lo, d_total=d)
     parts = [None] * world
@@ -64,7 +64,7 @@ def main():
     verdict = None
     try:
         capi.analyze_host(x[:, lo:hi], y[lo:hi], r[lo:hi], None, n_steps=20, device=local,
-                          k0=lo, d_total=d, precision=capi.FP64)
+                          k0=lo, d_total=d, precision=capi.FP64, sharded=True)
     except capi.TurbdaError as e:
         verdict = (e.code, e.diverged_particle, e.diverged_step)
     verdicts = [None] * world
@@ -89,13 +89,13 @@ def main():
     # per-step allreduce and the verdict min-reduce) instead of returning
     lo_e, hi_e = (0, d) if rank == 0 else (d, d)
     part_e = capi.analyze_host(x[:, lo_e:hi_e], y[lo_e:hi_e], 4.0, None, n_steps=20, joint=True,
-                               device=local, k0=lo_e, d_total=d, precision=capi.FP64)
+                               device=local, k0=lo_e, d_total=d, precision=capi.FP64, sharded=True)
     r_e = np.ones(d)
     r_e[7] = 1e-9
     verdict_e = None
     try:
         capi.analyze_host(x[:, lo_e:hi_e], y[lo_e:hi_e], r_e[lo_e:hi_e], None, n_steps=20,
-                          device=local, k0=lo_e, d_total=d, precision=capi.FP64)
+                          device=local, k0=lo_e, d_total=d, precision=capi.FP64, sharded=True)
     except capi.TurbdaError as e:
         verdict_e = (e.code, e.diverged_particle, e.diverged_step)
     verdicts_e = [None] * world
