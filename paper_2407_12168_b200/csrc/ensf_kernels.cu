@@ -306,8 +306,8 @@ __device__ __forceinline__ void fused_relax_epilogue(const KernelArgs& a, float*
         __syncthreads();
         TB_CHECK(a.tile_ticket != nullptr);
         if (threadIdx.x == 0) ticket = atomicAdd(a.tile_ticket + blockIdx.x, 1u);
-        TB_CHECK(ticket < gridDim.y);
         __syncthreads();
+        TB_CHECK(ticket < gridDim.y);
         if (ticket != gridDim.y - 1) return;  // not the last CTA of this tile
         __threadfence();
         if (threadIdx.x == 0) a.tile_ticket[blockIdx.x] = 0u;  // ready for the next launch
@@ -845,9 +845,17 @@ __global__ void obs_select_unique_kernel(const double* __restrict__ y, const dou
     ab[k] = make_double2(inv, y[q] * inv);
 }
 
-__global__ void iota_kernel(int32_t* __restrict__ v, int64_t n) {
+// (window-local index, position) pairs to sort: an index outside the window
+// [k0, k0 + dl) maps to the sentinel dl, so the keys span [0, dl] and the
+// radix sort only runs over bitwidth(dl) bits
+__global__ void window_keys_kernel(const int64_t* __restrict__ idx, int64_t n, int64_t k0,
+                                   int64_t dl, uint32_t* __restrict__ keys,
+                                   int32_t* __restrict__ pos) {
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (q < n) v[q] = int32_t(q);
+    if (q >= n) return;
+    const int64_t k = idx[q] - k0;
+    keys[q] = (k >= 0 && k < dl) ? uint32_t(k) : uint32_t(dl);
+    pos[q] = int32_t(q);
 }
 
 // Selection, any index order (duplicates add, as adjoint_scatter does,
@@ -855,16 +863,16 @@ __global__ void iota_kernel(int32_t* __restrict__ v, int64_t n) {
 // index; the head of every run of equal indices sums its run in observation
 // order.  No atomics: the sums are bitwise reproducible.
 __global__ void obs_select_runs_kernel(const double* __restrict__ y, const double* __restrict__ r,
-                                       int64_t r_stride, const int64_t* __restrict__ keys,
-                                       const int32_t* __restrict__ pos, int64_t obs_dim, int64_t k0,
+                                       int64_t r_stride, const uint32_t* __restrict__ keys,
+                                       const int32_t* __restrict__ pos, int64_t obs_dim,
                                        int64_t dl, double2* __restrict__ ab) {
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= obs_dim) return;
-    const int64_t key = keys[t];
+    const uint32_t key = keys[t];
     if (t > 0 && keys[t - 1] == key) return;
     TB_CHECK(pos[t] >= 0 && pos[t] < obs_dim);
-    const int64_t k = key - k0;
-    if (k < 0 || k >= dl) return;
+    const int64_t k = key;
+    if (k >= dl) return;  // outside the window
     double A = 0.0, B = 0.0;
     for (int64_t u = t; u < obs_dim && keys[u] == key; ++u) {
         const int64_t q = pos[u];
@@ -1009,7 +1017,8 @@ cudaError_t launch_f32_p(const KernelArgs& a, float* xt, const double2* ab,
     // config 4: 5588 -> 5922 ms), where the per-CTA prologue (fp64 loads,
     // the tile sort) repeated by every CTA of the tile and the last CTA's
     // relax of N x 64 values outweigh the two launches saved
-    const bool fused = !global_x && !a.minibatch && !exact && !unfused && ny <= 3;
+    static const bool fuse_all = env_int("TURBDA_F32_FUSE_ALL", 0) != 0;  // sweep knob
+    const bool fused = !global_x && !a.minibatch && !exact && !unfused && (ny <= 3 || fuse_all);
     // fused: + the sort staging columns, and room for the epilogue's
     // particles (nw P of them, which can exceed m by up to P - 1)
     const size_t smem =
@@ -1101,12 +1110,11 @@ cudaError_t launch_f64_p(const KernelArgs& a, const double* x, const double2* ab
 size_t obs_prep_scratch_bytes(int64_t obs_dim) {
     if (obs_dim <= 0) return 0;
     size_t tmp = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, static_cast<const int64_t*>(nullptr),
-                                    static_cast<int64_t*>(nullptr),
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, static_cast<const uint32_t*>(nullptr),
+                                    static_cast<uint32_t*>(nullptr),
                                     static_cast<const int32_t*>(nullptr),
                                     static_cast<int32_t*>(nullptr), obs_dim);
-    const size_t n = size_t(obs_dim);
-    return align256(8 * n) + 2 * align256(4 * n) + align256(tmp);
+    return 4 * align256(4 * size_t(obs_dim)) + align256(tmp);
 }
 
 cudaError_t launch_obs_prep(const double* y, const double* r, const int64_t* idx,
@@ -1121,7 +1129,7 @@ cudaError_t launch_obs_prep(const double* y, const double* r, const int64_t* idx
     }
     cudaError_t e = cudaMemsetAsync(ab, 0, sizeof(double2) * size_t(dl), st);
     if (e != cudaSuccess || obs_dim == 0) return e;
-    if (obs_dim > INT32_MAX) return cudaErrorInvalidValue;
+    if (obs_dim > INT32_MAX || dl >= int64_t(UINT32_MAX)) return cudaErrorInvalidValue;
     if (idx_increasing) {
         obs_select_unique_kernel<<<blocks_for(obs_dim, 256), 256, 0, st>>>(y, r, r_stride, idx,
                                                                           obs_dim, k0, dl, ab);
@@ -1129,19 +1137,24 @@ cudaError_t launch_obs_prep(const double* y, const double* r, const int64_t* idx
         return cudaGetLastError();
     }
     if (!scratch || scratch_bytes < obs_prep_scratch_bytes(obs_dim)) return cudaErrorInvalidValue;
-    const size_t n = size_t(obs_dim);
+    const size_t seg = align256(4 * size_t(obs_dim));
     unsigned char* b = static_cast<unsigned char*>(scratch);
-    int64_t* keys = reinterpret_cast<int64_t*>(b);
-    int32_t* pos_in = reinterpret_cast<int32_t*>(b + align256(8 * n));
-    int32_t* pos = reinterpret_cast<int32_t*>(b + align256(8 * n) + align256(4 * n));
-    void* tmp = b + align256(8 * n) + 2 * align256(4 * n);
-    size_t tmp_bytes = scratch_bytes - (align256(8 * n) + 2 * align256(4 * n));
-    iota_kernel<<<blocks_for(obs_dim, 256), 256, 0, st>>>(pos_in, obs_dim);
+    uint32_t* keys_in = reinterpret_cast<uint32_t*>(b);
+    uint32_t* keys = reinterpret_cast<uint32_t*>(b + seg);
+    int32_t* pos_in = reinterpret_cast<int32_t*>(b + 2 * seg);
+    int32_t* pos = reinterpret_cast<int32_t*>(b + 3 * seg);
+    void* tmp = b + 4 * seg;
+    size_t tmp_bytes = scratch_bytes - 4 * seg;
+    window_keys_kernel<<<blocks_for(obs_dim, 256), 256, 0, st>>>(idx, obs_dim, k0, dl, keys_in,
+                                                                pos_in);
+    int end_bit = 1;
+    while (end_bit < 32 && (uint64_t(1) << end_bit) <= uint64_t(dl)) ++end_bit;
     // LSD radix sort is stable: equal indices keep observation order
-    e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, idx, keys, pos_in, pos, obs_dim, 0, 64, st);
+    e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys_in, keys, pos_in, pos, obs_dim, 0,
+                                        end_bit, st);
     if (e != cudaSuccess) return e;
     obs_select_runs_kernel<<<blocks_for(obs_dim, 256), 256, 0, st>>>(y, r, r_stride, keys, pos,
-                                                                    obs_dim, k0, dl, ab);
+                                                                    obs_dim, dl, ab);
     add_launches(3);
     return cudaGetLastError();
 }
