@@ -959,6 +959,7 @@ bool f32_members_global(int m) { return sizeof(float) * 64 * size_t(m) > 200 * 1
 //                             shift first (no shift-free pass)
 //   TURBDA_F32_UNFUSED=1      prep_tiles -> ensf_f32 -> relax as three launches
 //                             (the same arithmetic: bit-identical output)
+//   TURBDA_F32_FUSE_ALL=1     the fused kernel also above 3 CTAs per tile
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
     return e ? std::atoi(e) : dflt;
@@ -1017,7 +1018,7 @@ cudaError_t launch_f32_p(const KernelArgs& a, float* xt, const double2* ab,
     // config 4: 5588 -> 5922 ms), where the per-CTA prologue (fp64 loads,
     // the tile sort) repeated by every CTA of the tile and the last CTA's
     // relax of N x 64 values outweigh the two launches saved
-    static const bool fuse_all = env_int("TURBDA_F32_FUSE_ALL", 0) != 0;  // sweep knob
+    static const bool fuse_all = env_int("TURBDA_F32_FUSE_ALL", 0) != 0;
     const bool fused = !global_x && !a.minibatch && !exact && !unfused && (ny <= 3 || fuse_all);
     // fused: + the sort staging columns, and room for the epilogue's
     // particles (nw P of them, which can exceed m by up to P - 1)

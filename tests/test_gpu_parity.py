@@ -522,3 +522,30 @@ def test_fused_kernel_bit_identical_to_three_launches(capi, tmp_path, m, d, stri
     fused = capi.analyze_host(x, y, 0.7, idx, n_steps=30, relax_factor=0.6)
     assert np.isfinite(fused).all()
     assert np.array_equal(fused, three)
+
+
+@pytest.mark.parametrize("m,d,stride", [(128, 2048 + 6, 3), (512, 640, 1), (200, 4700, 2)])
+def test_fused_kernel_at_many_ctas_per_tile_bit_identical(tmp_path, m, d, stride):
+    """Tiles spread over 4-8 CTAs (N = 128, 512 with 32-warp CTAs, 200) run
+    three launches by default; forced fused (TURBDA_F32_FUSE_ALL=1: the last
+    CTA of each tile relaxes it) they give the same bits."""
+    import os
+    import subprocess
+    import sys
+    x, y, idx, _ = conditioned_inputs(m, d, stride=stride)
+    np.save(tmp_path / "x.npy", x)
+    np.save(tmp_path / "y.npy", y)
+    np.save(tmp_path / "i.npy", idx if idx is not None else np.zeros(0, np.int64))
+    code = ("import numpy as np, sys; from paper_2407_12168_b200 import capi; "
+            "d = sys.argv[1]; x, y, i = (np.load(d + f) for f in ('/x.npy', '/y.npy', '/i.npy')); "
+            "i = i if i.size else None; "
+            "np.save(d + '/' + sys.argv[2], capi.analyze_host(x, y, 0.7, i, n_steps=30, "
+            "relax_factor=0.6))")
+    outs = []
+    for name, knob in (("fused.npy", "TURBDA_F32_FUSE_ALL"), ("three.npy", "TURBDA_F32_UNFUSED")):
+        env = dict(os.environ, **{knob: "1"})
+        subprocess.run([sys.executable, "-c", code, str(tmp_path), name], check=True, env=env,
+                       cwd=str(Path(__file__).resolve().parents[1]))
+        outs.append(np.load(tmp_path / name))
+    assert np.isfinite(outs[0]).all()
+    assert np.array_equal(outs[0], outs[1])
