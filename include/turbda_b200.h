@@ -14,6 +14,8 @@
  *   turbda_relax_spread   <- turbda::relax_spread     include/turbda/ensf.hpp:85-86,
  *                                                    src/ensf.cpp:225-258
  *   turbda_score          <- turbda::prior_score / posterior_score
+ *   turbda_likelihood_score <- turbda::likelihood_score  src/ensf.cpp:84-94
+ *   turbda_reverse_sde_step <- turbda::reverse_sde_step  src/ensf.cpp:108-130
  *                                                    include/turbda/ensf.hpp:52-70,
  *                                                    src/ensf.cpp:68-82,96-106
  *   turbda_diag           <- turbda::rmse / spread    include/turbda/ensemble.hpp:32-38,
@@ -193,6 +195,22 @@ TURBDA_API int turbda_score(const double* z, int64_t d, double t, const double* 
                  const int32_t* batch, int32_t n_batch, double eps, const double* y,
                  const double* r_diag, const int64_t* obs_idx, int64_t obs_dim, int32_t obs_kind,
                  double damping_t, double* out, int32_t device, turbda_status* status);
+
+/* likelihood_score (proj/src/ensf.cpp:84-94): H'^T R^-1 (y - h(z)) for the
+ * identity / index-selection (and arctan) operators, duplicates adding as
+ * adjoint_scatter does; host buffers, computed on the device. */
+TURBDA_API int turbda_likelihood_score(const double* z, int64_t d, const double* y,
+                            const double* r_diag, const int64_t* obs_idx, int64_t obs_dim,
+                            int32_t obs_kind, double* out, int32_t device,
+                            turbda_status* status);
+
+/* reverse_sde_step (proj/src/ensf.cpp:108-130): one Euler-Maruyama step of
+ * n particles [n][d] in place, z += -(b z - sigma^2 score) dt + sqrt(sigma^2
+ * dt) noise at pseudo-time t; host buffers, computed on the device.  A
+ * non-finite result returns TURBDA_DIVERGED (SamplerDivergedError(t)). */
+TURBDA_API int turbda_reverse_sde_step(double* particles, int32_t n, int64_t d, double t,
+                            double dt_pseudo, const double* scores, const double* noise,
+                            int32_t device, turbda_status* status);
 
 /* out[0] = sum_k (mean_k - truth_k)^2 (0 when truth == NULL),
  * out[1] = sum_{j,k} (x_jk - mean_k)^2.  members / truth are host or device

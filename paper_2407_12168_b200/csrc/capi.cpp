@@ -1315,6 +1315,98 @@ int turbda_score(const double* z, int64_t d, double t, const double* forecast, i
     return TURBDA_OK;
 }
 
+int turbda_likelihood_score(const double* z, int64_t d, const double* y, const double* r_diag,
+                            const int64_t* obs_idx, int64_t obs_dim, int32_t obs_kind, double* out,
+                            int32_t device, turbda_status* st) {
+    clear(st);
+    if (obs_kind < 0 || obs_kind > 3) return fail(st, TURBDA_CONFIG, "observation: unsupported operator kind");
+    if (d < 0 || obs_dim < 0 || (obs_dense(obs_kind) && obs_dim != d))
+        return fail(st, TURBDA_DIMENSION, "likelihood_score: dimension mismatch");
+    for (int64_t q = 0; q < obs_dim; ++q)
+        if (!(r_diag[q] > 0.0)) return fail(st, TURBDA_CONFIG, "observation: r_diag > 0");
+    if (!obs_dense(obs_kind))
+        for (int64_t q = 0; q < obs_dim; ++q)
+            if (obs_idx[q] < 0 || obs_idx[q] >= d)
+                return fail(st, TURBDA_DIMENSION, "observation: index outside the state");
+    int dev = 0;
+    if (int rc = resolve_device(device, st, &dev)) return rc;
+    TB_CUDA(cudaSetDevice(dev));
+    Workspace* w = workspace(dev);
+    std::lock_guard<std::mutex> lk(w->mu);
+    if (int rc = ws_init(w, st)) return rc;
+    cudaStream_t s = w->stream;
+    TB_CUDA(ws_acquire(w, s));
+    const size_t d1 = size_t(std::max<int64_t>(d, 1)), nb = size_t(std::max<int64_t>(obs_dim, 1));
+    TB_CUDA(w->z.reserve(sizeof(double) * d1));
+    TB_CUDA(w->out.reserve(sizeof(double) * d1));
+    TB_CUDA(w->y.reserve(sizeof(double) * nb));
+    TB_CUDA(w->r.reserve(sizeof(double) * nb));
+    TB_CUDA(w->idx.reserve(sizeof(int64_t) * nb));
+    TB_CUDA(w->ab.reserve(sizeof(double2) * d1));
+    TB_CUDA(cudaMemcpyAsync(w->z.p, z, sizeof(double) * size_t(d), cudaMemcpyHostToDevice, s));
+    if (obs_dim > 0) {
+        TB_CUDA(cudaMemcpyAsync(w->y.p, y, sizeof(double) * size_t(obs_dim), cudaMemcpyHostToDevice, s));
+        TB_CUDA(cudaMemcpyAsync(w->r.p, r_diag, sizeof(double) * size_t(obs_dim), cudaMemcpyHostToDevice, s));
+        if (!obs_dense(obs_kind))
+            TB_CUDA(cudaMemcpyAsync(w->idx.p, obs_idx, sizeof(int64_t) * size_t(obs_dim),
+                                    cudaMemcpyHostToDevice, s));
+    }
+    if (obs_dense(obs_kind))
+        TB_CUDA(launch_obs_prep(w->y.as<double>(), w->r.as<double>(), nullptr, d, obs_kind, 0, d,
+                                w->ab.as<double2>(), s, 1, true, nullptr, 0));
+    else if (int rc = select_prep(w, w->y.as<double>(), w->r.as<double>(), w->idx.as<int64_t>(),
+                                  obs_idx, obs_dim, obs_kind, 0, d, w->ab.as<double2>(), 1, s, st))
+        return rc;
+    TB_CUDA(launch_likelihood(w->z.as<double>(), d, w->ab.as<double2>(), obs_arctan(obs_kind) ? 1 : 0,
+                              w->out.as<double>(), s));
+    TB_CUDA(cudaMemcpyAsync(out, w->out.p, sizeof(double) * size_t(d), cudaMemcpyDeviceToHost, s));
+    TB_CUDA(cudaStreamSynchronize(s));
+    TB_CUDA(ws_release(w, s, false));
+    return TURBDA_OK;
+}
+
+int turbda_reverse_sde_step(double* particles, int32_t n, int64_t d, double t, double dt_pseudo,
+                            const double* scores, const double* noise, int32_t device,
+                            turbda_status* st) {
+    clear(st);
+    if (!(dt_pseudo > 0.0)) return fail(st, TURBDA_CONFIG, "reverse_sde_step: dt_pseudo > 0");
+    if (n < 0 || d < 0) return fail(st, TURBDA_DIMENSION, "reverse_sde_step: dimension mismatch");
+    int dev = 0;
+    if (int rc = resolve_device(device, st, &dev)) return rc;
+    TB_CUDA(cudaSetDevice(dev));
+    Workspace* w = workspace(dev);
+    std::lock_guard<std::mutex> lk(w->mu);
+    if (int rc = ws_init(w, st)) return rc;
+    cudaStream_t s = w->stream;
+    TB_CUDA(ws_acquire(w, s));
+    const size_t nd = size_t(n) * size_t(d), nd1 = std::max<size_t>(nd, 1);
+    TB_CUDA(w->x.reserve(sizeof(double) * nd1));
+    TB_CUDA(w->z.reserve(sizeof(double) * nd1));
+    TB_CUDA(w->out.reserve(sizeof(double) * nd1));
+    TB_CUDA(w->status.reserve(64));
+    unsigned int* bad = reinterpret_cast<unsigned int*>(w->status.as<unsigned char>() + 32);
+    TB_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned int), s));
+    TB_CUDA(cudaMemcpyAsync(w->z.p, particles, sizeof(double) * nd, cudaMemcpyHostToDevice, s));
+    TB_CUDA(cudaMemcpyAsync(w->x.p, scores, sizeof(double) * nd, cudaMemcpyHostToDevice, s));
+    TB_CUDA(cudaMemcpyAsync(w->out.p, noise, sizeof(double) * nd, cudaMemcpyHostToDevice, s));
+    // NoiseSchedule, proj/include/turbda/ensf.hpp:15-20
+    const double b = -1.0 / (1.0 - t);
+    const double s2 = 1.0 + 2.0 * t / (1.0 - t);
+    const double sig = std::sqrt(s2 * dt_pseudo);
+    TB_CUDA(launch_sde_step(w->z.as<double>(), int64_t(nd), w->x.as<double>(), w->out.as<double>(),
+                            b, s2, dt_pseudo, sig, bad, s));
+    unsigned int h_bad = 0;
+    TB_CUDA(cudaMemcpyAsync(particles, w->z.p, sizeof(double) * nd, cudaMemcpyDeviceToHost, s));
+    TB_CUDA(cudaMemcpyAsync(&h_bad, bad, sizeof(unsigned int), cudaMemcpyDeviceToHost, s));
+    TB_CUDA(cudaStreamSynchronize(s));
+    TB_CUDA(ws_release(w, s, false));
+    if (h_bad) {
+        if (st) st->diverged_t = t;
+        return fail(st, TURBDA_DIVERGED, "reverse SDE diverged at pseudo-time t=" + std::to_string(t));
+    }
+    return TURBDA_OK;
+}
+
 int turbda_diag(const double* members, int32_t m, int64_t d, const double* truth, double* out,
                 int32_t device, uint32_t flags, void* stream, turbda_status* st) {
     clear(st);

@@ -114,6 +114,13 @@ cudaError_t launch_relax_f32(const float* z, const double* x, int m, int64_t dl,
 cudaError_t launch_relax_f64(const double* z, const double* x, int m, int64_t dl,
                              double factor, double* out, cudaStream_t st);
 
+// likelihood_score / reverse_sde_step of the C++ API (host buffers staged)
+cudaError_t launch_likelihood(const double* z, int64_t d, const double2* ab, int obs_atan,
+                              double* out, cudaStream_t st);
+cudaError_t launch_sde_step(double* z, int64_t n, const double* sc, const double* xi, double b,
+                            double s2, double dt, double sig, unsigned int* bad,
+                            cudaStream_t st);
+
 // single-vector score (prior_score / posterior_score API), fp64 faithful
 cudaError_t launch_score_f64(const double* z, const double* x, int m, int64_t d,
                              const int32_t* batch, int nbatch, double alpha, double beta2,

@@ -883,6 +883,30 @@ __global__ void obs_select_runs_kernel(const double* __restrict__ y, const doubl
     ab[k] = make_double2(A, B);
 }
 
+// likelihood_score, proj/src/ensf.cpp:84-94: B - A z (or the arctan chain
+// rule) from the per-coordinate {A, B} of launch_obs_prep
+__global__ void likelihood_kernel(const double* __restrict__ z, int64_t d,
+                                  const double2* __restrict__ ab, int obs_atan,
+                                  double* __restrict__ out) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= d) return;
+    const double2 o = ab[k];
+    out[k] = obs_atan ? (o.y - o.x * atan(z[k])) / (1.0 + z[k] * z[k]) : o.y - o.x * z[k];
+}
+
+// reverse_sde_step, proj/src/ensf.cpp:108-130, evaluated as :126 writes it;
+// any non-finite result raises the flag
+__global__ void sde_step_kernel(double* __restrict__ z, int64_t n, const double* __restrict__ sc,
+                                const double* __restrict__ xi, double b, double s2, double dt,
+                                double sig, unsigned int* __restrict__ bad) {
+    const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    double v = z[q];
+    v += -(b * v - s2 * sc[q]) * dt + sig * xi[q];
+    z[q] = v;
+    if (!isfinite(v)) *bad = 1u;
+}
+
 // single-vector componentwise score, proj/src/ensf.cpp:33-64,96-106
 __global__ void score_kernel(const double* __restrict__ z, const double* __restrict__ x, int m,
                              int64_t d, const int32_t* __restrict__ batch, int nbatch,
@@ -1207,6 +1231,23 @@ cudaError_t launch_relax_f64(const double* z, const double* x, int m, int64_t dl
                              double factor, double* out, cudaStream_t st) {
     if (dl <= 0) return cudaSuccess;
     relax_kernel<double><<<blocks_for(dl, 256), 256, 0, st>>>(z, x, m, dl, factor, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_likelihood(const double* z, int64_t d, const double2* ab, int obs_atan,
+                              double* out, cudaStream_t st) {
+    if (d <= 0) return cudaSuccess;
+    likelihood_kernel<<<blocks_for(d, 256), 256, 0, st>>>(z, d, ab, obs_atan, out);
+    add_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sde_step(double* z, int64_t n, const double* sc, const double* xi, double b,
+                            double s2, double dt, double sig, unsigned int* bad,
+                            cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    sde_step_kernel<<<blocks_for(n, 256), 256, 0, st>>>(z, n, sc, xi, b, s2, dt, sig, bad);
+    add_launches(1);
     return cudaGetLastError();
 }
 

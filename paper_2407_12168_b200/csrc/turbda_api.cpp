@@ -307,16 +307,17 @@ std::vector<double> prior_score(const std::vector<double>& z, double t, const En
 std::vector<double> likelihood_score(const std::vector<double>& z, const Observation& obs) {
     obs.validate();
     if (z.size() != obs.op.state_dim) throw DimensionError("likelihood_score: dimension mismatch");
-    const std::vector<double> hz = apply_operator(obs.op, z);
-    std::vector<double> innov(hz.size());
-    for (std::size_t q = 0; q < hz.size(); ++q) innov[q] = (obs.y[q] - hz[q]) / obs.r_diag[q];
-    if (is_arctan(obs.op.kind)) {  // chain rule: d atan(x)/dx = 1 / (1 + x^2)
-        for (std::size_t q = 0; q < innov.size(); ++q) {
-            const double x = is_dense(obs.op.kind) ? z[q] : z[obs.op.indices[q]];
-            innov[q] /= 1.0 + x * x;
-        }
-    }
-    return adjoint_scatter(obs.op, innov);
+    // on the device: turbda_likelihood_score (the {A, B} observation prep of
+    // the analysis, duplicates adding as adjoint_scatter does)
+    std::vector<int64_t> idx(obs.op.indices.begin(), obs.op.indices.end());
+    std::vector<double> out(z.size());
+    turbda_status st;
+    const int rc = turbda_likelihood_score(z.data(), int64_t(z.size()), obs.y.data(),
+                                           obs.r_diag.data(), is_dense(obs.op.kind) ? nullptr : idx.data(),
+                                           int64_t(obs.y.size()), abi_kind(obs.op.kind), out.data(), -1,
+                                           &st);
+    check(rc, st);
+    return out;
 }
 
 std::vector<double> posterior_score(const std::vector<double>& z, double t,
@@ -338,18 +339,25 @@ void reverse_sde_step(std::vector<std::vector<double>>& particles, double t, dou
     if (dt_pseudo <= 0.0) throw ConfigError("reverse_sde_step: dt_pseudo > 0");
     if (scores.size() != particles.size() || noise.size() != particles.size())
         throw DimensionError("reverse_sde_step: array count mismatch");
-    const double b = NoiseSchedule::drift_b(t);
-    const double s2 = NoiseSchedule::sigma2(t);
-    const double sig = std::sqrt(s2 * dt_pseudo);
-    for (std::size_t i = 0; i < particles.size(); ++i) {
-        std::vector<double>& z = particles[i];
-        if (scores[i].size() != z.size() || noise[i].size() != z.size())
+    const size_t n = particles.size();
+    const size_t d = n ? particles[0].size() : 0;
+    for (size_t i = 0; i < n; ++i)
+        if (particles[i].size() != d || scores[i].size() != d || noise[i].size() != d)
             throw DimensionError("reverse_sde_step: dimension mismatch");
-        for (std::size_t k = 0; k < z.size(); ++k) {
-            z[k] += -(b * z[k] - s2 * scores[i][k]) * dt_pseudo + sig * noise[i][k];
-            if (!std::isfinite(z[k])) throw SamplerDivergedError(t);
-        }
+    // on the device (turbda_reverse_sde_step): pack [n][d], one launch
+    std::vector<double> z(n * d), sc(n * d), xi(n * d);
+    for (size_t i = 0; i < n; ++i) {
+        std::copy(particles[i].begin(), particles[i].end(), z.begin() + i * d);
+        std::copy(scores[i].begin(), scores[i].end(), sc.begin() + i * d);
+        std::copy(noise[i].begin(), noise[i].end(), xi.begin() + i * d);
     }
+    turbda_status st;
+    const int rc = turbda_reverse_sde_step(z.data(), int32_t(n), int64_t(d), t, dt_pseudo, sc.data(),
+                                           xi.data(), -1, &st);
+    if (rc != TURBDA_OK && rc != TURBDA_DIVERGED) check(rc, st);
+    for (size_t i = 0; i < n; ++i)
+        std::copy(z.begin() + i * d, z.begin() + (i + 1) * d, particles[i].begin());
+    if (rc == TURBDA_DIVERGED) throw SamplerDivergedError(t);
 }
 
 Ensemble analyze(const Ensemble& forecast, const Observation& obs, const EnsfConfig& cfg,

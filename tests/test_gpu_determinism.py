@@ -156,3 +156,44 @@ def test_pageable_staging_ring_matches_pinned_and_rows(capi):
     p = capi.params(d_total=d, d_local=d, obs_dim=d, n_members=m, n_steps=20, device=0)
     capi.analyze_rows(p, rp, y, np.ones(d), None, op)
     assert np.array_equal(np.stack(orows), page)
+
+
+def test_likelihood_score_and_sde_step_on_device(capi):
+    """The C++ API's likelihood_score / reverse_sde_step run on the device
+    (turbda_likelihood_score / turbda_reverse_sde_step, proj/src/ensf.cpp:
+    84-94,108-130): duplicates add as adjoint_scatter does; a non-finite step
+    reports SamplerDivergedError(t)."""
+    import ctypes as C
+    L = capi.lib()
+    vp = C.c_void_p
+    L.turbda_likelihood_score.argtypes = [vp, C.c_int64, vp, vp, vp, C.c_int64, C.c_int32, vp,
+                                          C.c_int32, C.POINTER(capi.Status)]
+    L.turbda_reverse_sde_step.argtypes = [vp, C.c_int32, C.c_int64, C.c_double, C.c_double, vp, vp,
+                                          C.c_int32, C.POINTER(capi.Status)]
+    g = np.random.default_rng(8)
+    d = 1000
+    z = g.standard_normal(d)
+    idx = np.array([3, 7, 7, 999, 3, 0], np.int64)
+    y = g.standard_normal(idx.size)
+    r = 0.5 + g.random(idx.size)
+    out = np.empty(d)
+    st = capi.Status()
+    assert L.turbda_likelihood_score(z.ctypes.data, d, y.ctypes.data, r.ctypes.data, idx.ctypes.data,
+                                     idx.size, 1, out.ctypes.data, 0, C.byref(st)) == capi.OK
+    want = np.zeros(d)
+    np.add.at(want, idx, (y - z[idx]) / r)
+    assert np.allclose(out, want, rtol=1e-13, atol=1e-15)
+    n, t, dt = 3, 0.4, 0.01
+    zz = g.standard_normal((n, d))
+    sc = g.standard_normal((n, d))
+    xi = g.standard_normal((n, d))
+    b, s2 = -1.0 / (1.0 - t), 1.0 + 2.0 * t / (1.0 - t)
+    want = zz + (-(b * zz - s2 * sc) * dt + np.sqrt(s2 * dt) * xi)
+    got = zz.copy()
+    assert L.turbda_reverse_sde_step(got.ctypes.data, n, d, t, dt, sc.ctypes.data, xi.ctypes.data, 0,
+                                     C.byref(st)) == capi.OK
+    assert np.allclose(got, want, rtol=1e-14, atol=1e-14)
+    sc[1, 5] = np.inf
+    assert L.turbda_reverse_sde_step(zz.ctypes.data, n, d, t, dt, sc.ctypes.data, xi.ctypes.data, 0,
+                                     C.byref(st)) == capi.DIVERGED
+    assert st.diverged_t == t
