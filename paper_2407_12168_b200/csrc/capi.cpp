@@ -204,6 +204,9 @@ struct Workspace {
     unsigned long long* status_host = nullptr;  // pinned
     void* comm = nullptr;                       // ncclComm_t (joint mode, sharded)
     int comm_world = 1;
+    void* jsym = nullptr;                       // symmetric-window joint buffer
+    void* jsym_win = nullptr;
+    size_t jsym_bytes = 0;
     DevBuf jpart, jred, jw;                     // joint-mode scratch
     std::vector<cudaStream_t> cstreams;         // host-mode chunk pipeline
     std::vector<cudaEvent_t> ev_chunk;
@@ -780,6 +783,13 @@ struct NcclApi {
                                ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
     const char* (*error_string)(ncclResult_t) = nullptr;
+    // NCCL >= 2.27 symmetric memory (optional): ncclMemAlloc'd buffers
+    // registered as a collective window let small allreduces take NCCL's
+    // symmetric (NVLS / load-store) kernels
+    ncclResult_t (*mem_alloc)(void**, size_t) = nullptr;
+    ncclResult_t (*mem_free)(void*) = nullptr;
+    ncclResult_t (*win_register)(ncclComm_t, void*, size_t, void**, int) = nullptr;
+    ncclResult_t (*win_deregister)(ncclComm_t, void*) = nullptr;
 };
 std::mutex g_nccl_mu;
 NcclApi g_nccl;
@@ -798,6 +808,12 @@ NcclApi* nccl_api() {
             g_nccl.error_string = reinterpret_cast<decltype(g_nccl.error_string)>(dlsym(h, "ncclGetErrorString"));
             g_nccl.ok = g_nccl.get_unique_id && g_nccl.comm_init_rank && g_nccl.comm_init_all &&
                         g_nccl.all_reduce && g_nccl.comm_destroy && g_nccl.error_string;
+            g_nccl.mem_alloc = reinterpret_cast<decltype(g_nccl.mem_alloc)>(dlsym(h, "ncclMemAlloc"));
+            g_nccl.mem_free = reinterpret_cast<decltype(g_nccl.mem_free)>(dlsym(h, "ncclMemFree"));
+            g_nccl.win_register =
+                reinterpret_cast<decltype(g_nccl.win_register)>(dlsym(h, "ncclCommWindowRegister"));
+            g_nccl.win_deregister =
+                reinterpret_cast<decltype(g_nccl.win_deregister)>(dlsym(h, "ncclCommWindowDeregister"));
         }
     }
     return g_nccl.ok ? &g_nccl : nullptr;
@@ -805,6 +821,52 @@ NcclApi* nccl_api() {
 
 int nccl_fail(turbda_status* st, NcclApi* api, ncclResult_t r, const char* where) {
     return fail(st, TURBDA_CUDA, std::string(where) + ": " + (api ? api->error_string(r) : "nccl"));
+}
+
+// collective, like the registration: every rank destroys its communicator
+void release_symmetric(Workspace* w, NcclApi* api) {
+    if (w->jsym_win && api->win_deregister)
+        api->win_deregister(static_cast<ncclComm_t>(w->comm), w->jsym_win);
+    if (w->jsym && api->mem_free) api->mem_free(w->jsym);
+    w->jsym = nullptr;
+    w->jsym_win = nullptr;
+    w->jsym_bytes = 0;
+}
+
+// The joint mode's per-step [G | nz | nx] buffer for a sharded call: with
+// NCCL symmetric memory, an ncclMemAlloc'd buffer registered once as a
+// symmetric window of the communicator (collective - every rank reaches this
+// point in the same call), else the plain workspace buffer.
+// TURBDA_NCCL_SYMMETRIC=0 forces the plain buffer.
+int joint_red_buffer(Workspace* w, NcclApi* api, void* comm, size_t bytes, turbda_status* st,
+                     double** out) {
+    static const bool sym_env = [] {
+        const char* e = std::getenv("TURBDA_NCCL_SYMMETRIC");
+        return !(e && std::atoi(e) == 0);
+    }();
+    const bool sym = sym_env && api && api->mem_alloc && api->mem_free && api->win_register &&
+                     api->win_deregister && w->comm && comm == w->comm;
+    if (!sym) {
+        TB_CUDA(w->jred.reserve(bytes));
+        *out = w->jred.as<double>();
+        return TURBDA_OK;
+    }
+    if (bytes > w->jsym_bytes) {
+        const ncclComm_t comm = static_cast<ncclComm_t>(w->comm);
+        if (w->jsym_win) api->win_deregister(comm, w->jsym_win);
+        if (w->jsym) api->mem_free(w->jsym);
+        w->jsym = nullptr;
+        w->jsym_win = nullptr;
+        w->jsym_bytes = 0;
+        const size_t want = (bytes + 4095) & ~size_t(4095);
+        ncclResult_t r = api->mem_alloc(&w->jsym, want);
+        if (r != ncclSuccess) return nccl_fail(st, api, r, "ncclMemAlloc");
+        r = api->win_register(comm, w->jsym, want, &w->jsym_win, NCCL_WIN_COLL_SYMMETRIC);
+        if (r != ncclSuccess) return nccl_fail(st, api, r, "ncclCommWindowRegister");
+        w->jsym_bytes = want;
+    }
+    *out = static_cast<double*>(w->jsym);
+    return TURBDA_OK;
 }
 
 // A window of a state sharded over ranks that share a communicator
@@ -909,7 +971,14 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
     TB_CUDA(w->z.reserve(sizeof(double) * md));
     TB_CUDA(w->ab.reserve(sizeof(double2) * size_t(std::max<int64_t>(dl, 1))));
     TB_CUDA(w->jpart.reserve(sizeof(double) * pl.scratch));
-    TB_CUDA(w->jred.reserve(sizeof(double) * pl.red_len));
+    double* red = nullptr;
+    if (comm) {
+        if (int rc = joint_red_buffer(w, nccl_api(), comm, sizeof(double) * pl.red_len, st, &red))
+            return rc;
+    } else {
+        TB_CUDA(w->jred.reserve(sizeof(double) * pl.red_len));
+        red = w->jred.as<double>();
+    }
     TB_CUDA(w->jw.reserve(sizeof(double) * size_t(m) * size_t(m)));
     TB_CUDA(w->status.reserve(64));
     unsigned long long* dstatus = w->status.as<unsigned long long>();
@@ -949,13 +1018,13 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
     for (int step = 0; step < p->n_steps; ++step) {
         const StepTimes& q = grid[size_t(step)];
         const StepF64 c{q.alpha, q.beta2, 1.0 / (2.0 * q.beta2), q.b, q.s2, q.damp, q.sig, q.dt};
-        TB_CUDA(launch_joint_gram(a, pl, z, dx, w->jpart.as<double>(), w->jred.as<double>(), s));
+        TB_CUDA(launch_joint_gram(a, pl, z, dx, w->jpart.as<double>(), red, s));
         if (comm) {
-            ncclResult_t rr = api->all_reduce(w->jred.p, w->jred.p, pl.red_len, ncclDouble, ncclSum,
+            ncclResult_t rr = api->all_reduce(red, red, pl.red_len, ncclDouble, ncclSum,
                                               static_cast<ncclComm_t>(comm), s);
             if (rr != ncclSuccess) return nccl_fail(st, api, rr, "ncclAllReduce");
         }
-        TB_CUDA(launch_joint_update(a, dx, w->ab.as<double2>(), w->jred.as<double>(), w->jw.as<double>(),
+        TB_CUDA(launch_joint_update(a, dx, w->ab.as<double2>(), red, w->jw.as<double>(),
                                     c, step, z, dstatus, p->precision == TURBDA_FP32, s));
     }
     if (prof.a) {
@@ -1008,10 +1077,12 @@ int join_empty_window(const turbda_ensf_params* p, int device, cudaStream_t user
     const ncclComm_t comm = static_cast<ncclComm_t>(w->comm);
     if (p->score_mode == TURBDA_SCORE_JOINT) {
         const JointPlan pl = joint_plan(p->n_members, p->n_members, 1);
-        TB_CUDA(w->jred.reserve(sizeof(double) * pl.red_len));
+        double* red = nullptr;
+        if (int rc = joint_red_buffer(w, api, w->comm, sizeof(double) * pl.red_len, st, &red))
+            return rc;
         for (int step = 0; step < p->n_steps; ++step) {
-            TB_CUDA(cudaMemsetAsync(w->jred.p, 0, sizeof(double) * pl.red_len, s));
-            const ncclResult_t r = api->all_reduce(w->jred.p, w->jred.p, pl.red_len, ncclDouble,
+            TB_CUDA(cudaMemsetAsync(red, 0, sizeof(double) * pl.red_len, s));
+            const ncclResult_t r = api->all_reduce(red, red, pl.red_len, ncclDouble,
                                                    ncclSum, comm, s);
             if (r != ncclSuccess) return nccl_fail(st, api, r, "ncclAllReduce");
         }
@@ -1474,6 +1545,7 @@ int turbda_comm_init(int32_t device, int32_t rank, int32_t world, const void* id
     Workspace* w = workspace(dev);
     std::lock_guard<std::mutex> lk(w->mu);
     if (w->comm) {
+        release_symmetric(w, api);
         api->comm_destroy(static_cast<ncclComm_t>(w->comm));
         w->comm = nullptr;
     }
@@ -1492,7 +1564,10 @@ int turbda_comm_destroy(int32_t device) {
     Workspace* w = workspace(device);
     std::lock_guard<std::mutex> lk(w->mu);
     NcclApi* api = nccl_api();
-    if (w->comm && api) api->comm_destroy(static_cast<ncclComm_t>(w->comm));
+    if (w->comm && api) {
+        release_symmetric(w, api);
+        api->comm_destroy(static_cast<ncclComm_t>(w->comm));
+    }
     w->comm = nullptr;
     w->comm_world = 1;
     return TURBDA_OK;
