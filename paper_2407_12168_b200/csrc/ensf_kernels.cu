@@ -1034,8 +1034,10 @@ cudaError_t launch_f32_p(const KernelArgs& a, float* xt, const double2* ab,
     const size_t smem_sm = size_t(227) * 1024;
     const bool wide = sorted && !exact && tile * 2 > smem_sm;  // one tile per SM
     const int wmax = wide ? 32 : 8;
-    const int nw = groups < wmax ? groups : wmax;
-    const unsigned ny = unsigned((groups + nw - 1) / nw);
+    // fewest CTAs per tile, warps spread evenly over them (N = 20 at P = 1:
+    // 3 CTAs of 7 warps instead of 8 + 8 + 4 with 4 idle warps)
+    const unsigned ny = unsigned((groups + wmax - 1) / wmax);
+    const int nw = int((groups + ny - 1) / ny);
     // fused when a tile spans at most 3 CTAs: measured faster there (config
     // 3: 1 CTA, 190.3 -> 188.0 ms; config 1: 3 CTAs, 0.109 -> 0.104 ms;
     // config 2: 2 CTAs, equal) and slower at 4 (config 5: 744 -> 756 ms,
