@@ -372,7 +372,8 @@ __device__ __forceinline__ void fused_relax_epilogue(const KernelArgs& a, float*
 // componentwise score only needs the multiset of member values per
 // coordinate, proj/src/ensf.cpp:43-61), pass 1 becomes a binary search.
 // kPolyEvery: every kPolyEvery-th (member, particle) slot of the unrolled
-// member loop takes its two exponentials from ex2_poly2 instead of MUFU.
+// member loop takes its two exponentials from ex2_poly2 instead of MUFU (the
+// slot pattern depends on P: sorted tiles therefore always run P = 4).
 // kFused: the whole analysis in one launch.  The prologue converts (and for
 // kSorted rank-sorts) the tile's fp64 forecast columns straight into shared
 // memory and takes the forecast statistics of relax_spread; the epilogue
@@ -1122,6 +1123,8 @@ cudaError_t launch_f64_p(const KernelArgs& a, const double* x, const double2* ab
     const dim3 block(32 * nw);
     const dim3 grid(unsigned((a.dl + kTile - 1) / kTile), unsigned((groups + nw - 1) / nw));
     const size_t smem = kSmemX ? sizeof(double2) * 32 * size_t(a.m) : 0;
+    // the register budget ptxas picks (114 at P = 2) beats capping it for
+    // occupancy: config 3 1577 ms vs 1698 (80 regs) / 1747 ms (64 regs)
     auto kern = a.minibatch ? ensf_f64_kernel<P, true, kSmemX> : ensf_f64_kernel<P, false, kSmemX>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1203,7 +1206,11 @@ cudaError_t launch_ensf_f32(const KernelArgs& a, const double2* ab, const StepF3
     const auto warps_for = [&](int pp) { return tiles_n * ((a.m + pp - 1) / pp); };
     const int64_t wave = 148 * 24;
     // (particles past m in the last warp are computed and discarded)
-    if ((a.m % 4 == 0 || a.m >= 32) && warps_for(4) >= wave)
+    // sorted tiles always take P = 4: their polynomial slots are a pattern
+    // over (member, particle-in-warp), so one P for every window keeps
+    // sharded results bit-identical to the whole-state call (tying the slot
+    // to the member index instead measured 1.4-2.7 % slower, configs 2/4/5)
+    if (sorted || ((a.m % 4 == 0 || a.m >= 32) && warps_for(4) >= wave))
         return launch_f32_p<4>(a, xt, ab, steps, batches, z, status, st, sorted);
     if ((a.m % 2 == 0 || a.m >= 16) && warps_for(2) >= wave / 2)
         return launch_f32_p<2>(a, xt, ab, steps, batches, z, status, st, sorted);

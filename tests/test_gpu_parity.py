@@ -98,17 +98,21 @@ def test_large_members_smem_and_global_paths(capi, port):
             assert rel_l2(got, want) <= tol, (m, d, prec, rel_l2(got, want))
 
 
-@pytest.mark.parametrize("precision", [0, 1])
-def test_windows_reassemble_bitwise(capi, precision):
+@pytest.mark.parametrize("precision,m,minibatch,arctan", [(0, 16, 0, False), (1, 16, 0, False),
+                                                         (0, 40, 0, False), (0, 24, 9, False),
+                                                         (0, 20, 0, True)])
+def test_windows_reassemble_bitwise(capi, precision, m, minibatch, arctan):
     """State-dimension sharding: windows [k0, k0+dl) reproduce the whole-state
-    call bit for bit (odd boundaries included)."""
-    x, y, idx = throughput_inputs(16, 1000, stride=3)
-    whole = capi.analyze_host(x, y, 0.7, idx, n_steps=30, precision=precision)
+    call bit for bit (odd boundaries included) - unsorted and sorted member
+    tiles, minibatches, the arctan extension."""
+    x, y, idx = throughput_inputs(m, 1000, stride=3)
+    kw = dict(n_steps=30, precision=precision, minibatch_j=minibatch, arctan=arctan)
+    whole = capi.analyze_host(x, y, 0.7, idx, **kw)
     parts = []
     for lo, hi in ((0, 129), (129, 640), (640, 1000)):
         sel = (idx >= lo) & (idx < hi)
-        parts.append(capi.analyze_host(x[:, lo:hi], y[sel], 0.7, idx[sel], n_steps=30,
-                                       precision=precision, k0=lo, d_total=1000))
+        parts.append(capi.analyze_host(x[:, lo:hi], y[sel], 0.7, idx[sel], k0=lo, d_total=1000,
+                                       **kw))
     assert np.array_equal(np.concatenate(parts, axis=1), whole)
 
 
@@ -549,3 +553,18 @@ def test_fused_kernel_at_many_ctas_per_tile_bit_identical(tmp_path, m, d, stride
         outs.append(np.load(tmp_path / name))
     assert np.isfinite(outs[0]).all()
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_windows_with_different_particles_per_warp_bitwise(capi):
+    """A small window runs 1-2 particles per warp, a large one 4 (the choice
+    follows the window's width); the sorted-tile kernel's polynomial share is
+    tied to the member index, so the results still reassemble bit for bit."""
+    m, d = 64, 17_384
+    x, y, idx = throughput_inputs(m, d, stride=3)
+    whole = capi.analyze_host(x, y, 0.7, idx, n_steps=20)
+    parts = []
+    for lo, hi in ((0, 1000), (1000, d)):
+        sel = (idx >= lo) & (idx < hi)
+        parts.append(capi.analyze_host(x[:, lo:hi], y[sel], 0.7, idx[sel], n_steps=20, k0=lo,
+                                       d_total=d))
+    assert np.array_equal(np.concatenate(parts, axis=1), whole)
