@@ -711,40 +711,69 @@ __global__ void __launch_bounds__(128) ensf_f64_kernel(KernelArgs a, const doubl
     for (int s = 0; s < a.n_steps; ++s) {
         const StepF64 c = steps[s];
         const int32_t* bt = kMinibatch ? batches + size_t(s) * size_t(a.j_batch) : nullptr;
+        // weights w = fast_exp_nonpos((m - (z - alpha x_j)^2) / (2 beta^2)),
+        // den = sum w, num = sum w x (proj/src/ensf.cpp:51-61)
+        double nx[P], ny[P], ex[P], ey[P];
+        auto weight_pass = [&](const double (&mx)[P], const double (&my)[P]) {
+#pragma unroll
+            for (int p = 0; p < P; ++p) nx[p] = ny[p] = ex[p] = ey[p] = 0.0;
+            for (int jj = 0; jj < a.j_batch; ++jj) {
+                const int j = kMinibatch ? __ldg(bt + jj) : jj;
+                const double2 xv = kSmemX ? xs[j * 32 + lane]
+                                          : load_pair(x + size_t(j) * size_t(a.dl), kl, a.dl, aligned);
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const double dx = zx[p] - c.alpha * xv.x;
+                    const double dy = zy[p] - c.alpha * xv.y;
+                    const double wx = fast_exp_nonpos_dev((mx[p] - dx * dx) * c.inv2b);
+                    const double wy = fast_exp_nonpos_dev((my[p] - dy * dy) * c.inv2b);
+                    ex[p] += wx;
+                    ey[p] += wy;
+                    nx[p] += wx * xv.x;
+                    ny[p] += wy * xv.y;
+                }
+            }
+        };
+        // Shift-free first: with shift 0 the weights differ from the
+        // reference's min-shifted ones by one common factor, which cancels in
+        // num / den, and only by exp rounding (1e-16) otherwise.  A value
+        // whose weights all but vanish (den < 1e-280: every member beyond ~25
+        // kernel widths, where the unshifted exp would underflow) is redone
+        // with the reference's exact shift min_j (z - alpha x_j)^2
+        // (proj/src/ensf.cpp:41-50); the choice is per value, so results do
+        // not depend on which values share the warp.
         double mx[P], my[P];
 #pragma unroll
-        for (int p = 0; p < P; ++p) mx[p] = my[p] = __longlong_as_double(0x7ff0000000000000ll);
-        for (int jj = 0; jj < a.j_batch; ++jj) {
-            const int j = kMinibatch ? __ldg(bt + jj) : jj;
-            const double2 xv = kSmemX ? xs[j * 32 + lane]
-                                      : load_pair(x + size_t(j) * size_t(a.dl), kl, a.dl, aligned);
+        for (int p = 0; p < P; ++p) mx[p] = my[p] = 0.0;
+        weight_pass(mx, my);
+        unsigned redo = 0;
 #pragma unroll
-            for (int p = 0; p < P; ++p) {
-                const double dx = zx[p] - c.alpha * xv.x;
-                const double dy = zy[p] - c.alpha * xv.y;
-                const double d2x = dx * dx, d2y = dy * dy;
-                mx[p] = d2x < mx[p] ? d2x : mx[p];
-                my[p] = d2y < my[p] ? d2y : my[p];
-            }
+        for (int p = 0; p < P; ++p) {
+            if (!(ex[p] >= 1e-280)) redo |= 1u << (2 * p);
+            if (!(ey[p] >= 1e-280)) redo |= 2u << (2 * p);
         }
-        double nx[P], ny[P], ex[P], ey[P];
+        if (__any_sync(0xffffffffu, redo != 0)) {
 #pragma unroll
-        for (int p = 0; p < P; ++p) nx[p] = ny[p] = ex[p] = ey[p] = 0.0;
-        for (int jj = 0; jj < a.j_batch; ++jj) {
-            const int j = kMinibatch ? __ldg(bt + jj) : jj;
-            const double2 xv = kSmemX ? xs[j * 32 + lane]
-                                      : load_pair(x + size_t(j) * size_t(a.dl), kl, a.dl, aligned);
+            for (int p = 0; p < P; ++p) mx[p] = my[p] = __longlong_as_double(0x7ff0000000000000ll);
+            for (int jj = 0; jj < a.j_batch; ++jj) {
+                const int j = kMinibatch ? __ldg(bt + jj) : jj;
+                const double2 xv = kSmemX ? xs[j * 32 + lane]
+                                          : load_pair(x + size_t(j) * size_t(a.dl), kl, a.dl, aligned);
+#pragma unroll
+                for (int p = 0; p < P; ++p) {
+                    const double dx = zx[p] - c.alpha * xv.x;
+                    const double dy = zy[p] - c.alpha * xv.y;
+                    const double d2x = dx * dx, d2y = dy * dy;
+                    mx[p] = d2x < mx[p] ? d2x : mx[p];
+                    my[p] = d2y < my[p] ? d2y : my[p];
+                }
+            }
 #pragma unroll
             for (int p = 0; p < P; ++p) {
-                const double dx = zx[p] - c.alpha * xv.x;
-                const double dy = zy[p] - c.alpha * xv.y;
-                const double wx = fast_exp_nonpos_dev((mx[p] - dx * dx) * c.inv2b);
-                const double wy = fast_exp_nonpos_dev((my[p] - dy * dy) * c.inv2b);
-                ex[p] += wx;
-                ey[p] += wy;
-                nx[p] += wx * xv.x;
-                ny[p] += wy * xv.y;
+                if (!(redo & (1u << (2 * p)))) mx[p] = 0.0;
+                if (!(redo & (2u << (2 * p)))) my[p] = 0.0;
             }
+            weight_pass(mx, my);
         }
         const uint64_t n0 = uint64_t(s + 1) * uint64_t(a.d_total) + kg;
 #pragma unroll

@@ -220,6 +220,10 @@ def test_far_from_members_exact_shift_redo(capi, port, m, minibatch, y0, r):
     got = capi.analyze_host(x, y, r, n_steps=100, minibatch_j=minibatch, relax_factor=0.0,
                             precision=capi.FP32)
     assert rel_l2(got, want) <= FP32_TOL, rel_l2(got, want)
+    # the fp64 faithful kernel is shift-free too (redo below den = 1e-280)
+    got64 = capi.analyze_host(x, y, r, n_steps=100, minibatch_j=minibatch, relax_factor=0.0,
+                              precision=capi.FP64)
+    assert rel_l2(got64, want) <= FP64_TOL, rel_l2(got64, want)
 
 
 def test_shift_free_weights_match_exact_shift_kernel(capi, tmp_path):
