@@ -1122,13 +1122,16 @@ cudaError_t launch_f32_p(const KernelArgs& a, float* xt, const double2* ab,
         return a.minibatch ? go(ensf_f32_kernel<P, true, false, 0, 3, true>)
                            : go(ensf_f32_kernel<P, false, false, 0, 3, true>);
     if (a.minibatch) return go(ensf_f32_kernel<P, true, false, 0, 3>);
-    if (exact)
-        return sorted ? go(ensf_f32_kernel<P, false, true, 0, 3, false, 256, false>)
-                      : go(ensf_f32_kernel<P, false, false, 0, 4, false, 256, false>);
     if (!sorted) {
+        if (exact) return go(ensf_f32_kernel<P, false, false, 0, 4, false, 256, false>);
         return fused ? go(ensf_f32_kernel<P, false, false, kPolyUnsorted, 4, false, 256, true, true>)
                      : go(ensf_f32_kernel<P, false, false, kPolyUnsorted, 4>);
     }
+    // sorted member tiles always run P = 4 (launch_ensf_f32)
+    if constexpr (P != 4) {
+        return cudaErrorInvalidValue;
+    } else {
+    if (exact) return go(ensf_f32_kernel<P, false, true, 0, 3, false, 256, false>);
     if (wide)
         return fused ? go(ensf_f32_kernel<P, false, true, kPolySorted, 1, false, 1024, true, true>)
                      : go(ensf_f32_kernel<P, false, true, kPolySorted, 1, false, 1024>);
@@ -1141,6 +1144,7 @@ cudaError_t launch_f32_p(const KernelArgs& a, float* xt, const double2* ab,
     }
     return fused ? go(ensf_f32_kernel<P, false, true, 0, 3, false, 256, true, true>)
                  : go(ensf_f32_kernel<P, false, true, 0, 3>);
+    }
 }
 
 template <int P, bool kSmemX>
