@@ -550,6 +550,11 @@ def main():
         except ValueError:
             traffic = None
     pair_evals = units_per_launch * m
+    # sorted member tiles take 1/8 of the exponentials on the FMA pipe when
+    # four tiles fit an SM (24 < N <~ 200) or one 32-warp CTA holds one
+    # (440 <~ N <~ 800); ensf_kernels.cu launch_f32_p
+    poly_share = 0.125 if (not joint and (24 < m <= 200 or 440 <= m <= 800)) else 0.0
+    xu_ops_per_unit = m * (1.0 - poly_share) + 2.0
     mufu_peak = MUFU_PER_CLK_PER_SM * 148 * pk.get("sm_max_mhz", 1965.0) * 1e6
     fp64_peak = 64 * 2 * 148 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
     roofline = {
@@ -566,7 +571,21 @@ def main():
             "peak": mufu_peak, "frac": pair_evals / (kern_ms / 1e3) / mufu_peak,
             "peak_source": "16 ex2/clk/SM measured x 148 SMs x sm_max_mhz",
             "note": "MUFU-only ceiling; a share of the exponentials comes from an FMA-pipe "
-                    "polynomial (DESIGN.md section 3), so the kernel can pass 1.0"} if not joint else {
+                    "polynomial (DESIGN.md section 3), so the kernel can pass 1.0",
+            # every op the kernel issues to the XU (MUFU) pipe: the exponentials
+            # left on MUFU plus lg2, sqrt, sin, cos of the Box-Muller noise (2 per
+            # unit), each 8 cycles per warp-instruction per SM partition
+            # (tools/mufu_ops_microbench.cu)
+            "xu_ops_per_unit": xu_ops_per_unit,
+            "xu_pipe_frac": units_per_launch * xu_ops_per_unit / (kern_ms / 1e3) / mufu_peak}
+            if not joint and prec == capi.FP32 else {
+            "bound": "fp64 pipe (the reference's fast_exp_nonpos + the weight sums, ~25 fp64 "
+                     "ops per pair-eval; ncu: profiles/r02_ncu_full_cfg3_f64.md)",
+            "achieved": pair_evals / (kern_ms / 1e3), "unit": "pair-evals/s",
+            "peak": fp64_peak * 1e12 / 2.0 / 25.0,
+            "frac": pair_evals / (kern_ms / 1e3) / (fp64_peak * 1e12 / 2.0 / 25.0),
+            "peak_source": "64 fp64 ops/clk/SM x 148 x sm_max_mhz / 25 ops per pair-eval"}
+            if not joint else {
             "bound": "fp64 pipe (Gram + weighted sum: 2 DFMA per pair-eval)",
             "achieved": 4.0 * pair_evals / (kern_ms / 1e3) / 1e12, "unit": "TFLOP/s",
             "peak": fp64_peak, "frac": 4.0 * pair_evals / (kern_ms / 1e3) / 1e12 / fp64_peak,
