@@ -384,7 +384,7 @@ __device__ __forceinline__ void fused_relax_epilogue(const KernelArgs& a, float*
 // prep_tiles / relax launches.
 template <int P, bool kMinibatch, bool kSorted, int kPolyEvery, int kMinBlocks = 1,
           bool kGlobalX = false, int kThreads = 256, bool kShiftFree = true, bool kFused = false,
-          bool kNewtonRcp = true>
+          bool kNewtonRcp = true, int kJ = 0>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelArgs a, const float* __restrict__ xt,
                                                        const double2* __restrict__ ab,
                                                        const StepF32* __restrict__ steps,
@@ -394,6 +394,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
     static_assert(!(kMinibatch && kSorted), "minibatches use the two-pass member loop");
     static_assert(!(kGlobalX && kSorted), "very large ensembles use the two-pass member loop");
     static_assert(!(kFused && (kGlobalX || kMinibatch)), "fused: shared-memory tiles, no minibatch");
+    static_assert(kJ == 0 || !(kMinibatch || kSorted || kGlobalX), "compile-time J: unsorted tiles");
     constexpr int U = 4;  // member-loop unroll
     extern __shared__ float4 smem[];
     // the tile's members: shared memory, or (ensembles too large for it)
@@ -463,6 +464,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
         const StepF32 c = load_step(steps + s);
         const float2 nas2 = f2(c.nas);
         const int32_t* bt = kMinibatch ? batches + size_t(s) * size_t(a.j_batch) : nullptr;
+        const uint64_t n0 = uint64_t(s + 1) * uint64_t(a.d_total) + kg;
+        // compile-time J: the step's noise is drawn first, in the same basic
+        // block as the fully unrolled member loop, so ptxas interleaves the
+        // Philox / Box-Muller chain with the exponentials (n0 even: the host
+        // picks these kernels only for even d_total and k0)
+        float2 xi_early[kJ > 0 ? P : 1];
+        if constexpr (kJ > 0) {
+#pragma unroll
+            for (int p = 0; p < P; ++p)
+                xi_early[p] = box_muller_f32(philox_block_rk(n0 >> 1, uint32_t(i0 + p), a.cycle_lo, a.rk));
+        }
 
         // u_j = s (z - alpha x_j): one FFMA2 per member and coordinate pair
         float2 zs[P];
@@ -477,6 +489,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
             for (int p = 0; p < P; ++p) {
                 den[p] = f2(0.f);
                 num[p] = f2(0.f);
+            }
+            if constexpr (kJ > 0) {
+#pragma unroll
+                for (int j = 0; j < kJ; ++j) {
+                    const float2 xv = xs[j * 32 + lane];
+#pragma unroll
+                    for (int p = 0; p < P; ++p) {
+                        const float2 u = __ffma2_rn(nas2, xv, zs[p]);
+                        const float2 e = __ffma2_rn(make_float2(-u.x, -u.y), u, m2[p]);
+                        const float2 w = make_float2(ex2f(e.x), ex2f(e.y));
+                        den[p] = __fadd2_rn(den[p], w);
+                        num[p] = __ffma2_rn(w, u, num[p]);
+                    }
+                }
+                return;
             }
             int jj = 0;
             for (; jj + U <= a.j_batch; jj += U) {
@@ -569,7 +596,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
             weight_pass(m2, den, num);
         }
         // posterior score + Euler-Maruyama, proj/src/ensf.cpp:197-214
-        const uint64_t n0 = uint64_t(s + 1) * uint64_t(a.d_total) + kg;
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             // num / den per coordinate: a merged 1 / (den.x den.y) saves a
@@ -584,7 +610,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
             } else {
                 lik = __ffma2_rn(nA2, z[p], B2);
             }
-            const float2 xi = normal_pair_f32(n0, uint32_t(i0 + p), a.cycle_lo, a.rk);
+            float2 xi;
+            if constexpr (kJ > 0) xi = xi_early[p];
+            else xi = normal_pair_f32(n0, uint32_t(i0 + p), a.cycle_lo, a.rk);
             float2 zn = __ffma2_rn(z[p], f2(c.nbdt), z[p]);
             zn = __ffma2_rn(f2(c.kp), q, zn);
             zn = __ffma2_rn(f2(c.kl), lik, zn);
@@ -1124,6 +1152,12 @@ cudaError_t launch_f32_p(const KernelArgs& a, float* xt, const double2* ab,
     if (a.minibatch) return go(ensf_f32_kernel<P, true, false, 0, 3>);
     if (!sorted) {
         if (exact) return go(ensf_f32_kernel<P, false, false, 0, 4, false, 256, false>);
+        static const int j20 = env_int("TURBDA_F32_J20", 0);
+        if (j20 && fused && a.j_batch == 20 && ((a.d_total | a.k0) & 1) == 0) {
+            if (j20 == 1) return go(ensf_f32_kernel<P, false, false, 0, 4, false, 256, true, true, true, 20>);
+            if (j20 == 2) return go(ensf_f32_kernel<P, false, false, 0, 3, false, 256, true, true, true, 20>);
+            if (j20 == 3) return go(ensf_f32_kernel<P, false, false, 0, 2, false, 256, true, true, true, 20>);
+        }
         return fused ? go(ensf_f32_kernel<P, false, false, kPolyUnsorted, 4, false, 256, true, true>)
                      : go(ensf_f32_kernel<P, false, false, kPolyUnsorted, 4>);
     }
@@ -1243,6 +1277,9 @@ cudaError_t launch_ensf_f32(const KernelArgs& a, const double2* ab, const StepF3
     // over (member, particle-in-warp), so one P for every window keeps
     // sharded results bit-identical to the whole-state call (tying the slot
     // to the member index instead measured 1.4-2.7 % slower, configs 2/4/5)
+    static const int force_p = env_int("TURBDA_F32_FORCE_P", 0);
+    if (!sorted && force_p == 1) return launch_f32_p<1>(a, xt, ab, steps, batches, z, status, st, sorted);
+    if (!sorted && force_p == 2) return launch_f32_p<2>(a, xt, ab, steps, batches, z, status, st, sorted);
     if (sorted || ((a.m % 4 == 0 || a.m >= 32) && warps_for(4) >= wave))
         return launch_f32_p<4>(a, xt, ab, steps, batches, z, status, st, sorted);
     if ((a.m % 2 == 0 || a.m >= 16) && warps_for(2) >= wave / 2)
