@@ -580,7 +580,13 @@ int run_slice(const turbda_ensf_params* p, const Window& win, int device, const 
         xt_total += fp32 ? ensf_f32_scratch_bytes(m, c.dl) : 0;
         tk_total += fp32 ? ensf_f32_ticket_bytes(c.dl) : 0;
     }
-    TB_CUDA(w->ticket.reserve(std::max<size_t>(tk_total, 1)));
+    {
+        // the fused kernel's per-tile tickets start at zero and each tile's
+        // last CTA resets its own, so only a fresh allocation is cleared
+        const void* before = w->ticket.p;
+        TB_CUDA(w->ticket.reserve(std::max<size_t>(tk_total, 1)));
+        if (w->ticket.p != before) TB_CUDA(cudaMemsetAsync(w->ticket.p, 0, w->ticket.cap, s));
+    }
     TB_CUDA(w->z.reserve((fp32 ? sizeof(float) : sizeof(double)) * std::max<size_t>(md, 1)));
     TB_CUDA(w->xt.reserve(std::max<size_t>(xt_total, 1)));
     TB_CUDA(w->ab.reserve(sizeof(double2) * size_t(std::max<int64_t>(dl, 1))));

@@ -1073,6 +1073,8 @@ cudaError_t launch_kernel(K kern, dim3 grid, dim3 block, size_t smem, cudaStream
 //    polynomial shares, 80-register and 32-48-register budgets, P = 1 / 2
 //    and Box-Muller on the FMA pipe all measured slower or equal at config
 //    3: the kernel sits at 86 % of the MUFU pipe, profiles/r02_sweeps.md);
+//  * grids under a wave (config 1): P = 1 in 4-warp CTAs, and at N = 20 the
+//    compile-time member loop with the noise drawn inside it;
 //  * all of these fused: one launch per analysis;
 //  * minibatches and ensembles whose tile exceeds shared memory: the
 //    two-pass member loop, all MUFU, unfused.
@@ -1091,19 +1093,25 @@ cudaError_t launch_f32_p(const KernelArgs& a, float* xt, const double2* ab,
     const size_t tile = sizeof(float) * kTile * size_t(a.m);
     const size_t smem_sm = size_t(227) * 1024;
     const bool wide = sorted && !exact && tile * 2 > smem_sm;  // one tile per SM
-    const int wmax = wide ? 32 : 8;
+    // P = 1 (grids under a wave): 4-warp CTAs spread a tile's particles over
+    // more SMs (config 1: 5 CTAs per tile, 4.3 per SM; 8-warp CTAs leave 60
+    // SMs with 2 CTAs and 88 with 3)
+    const int wmax = wide ? 32 : (P == 1 && !sorted) ? 4 : 8;
     // fewest CTAs per tile, warps spread evenly over them (N = 20 at P = 1:
     // 3 CTAs of 7 warps instead of 8 + 8 + 4 with 4 idle warps)
     const unsigned ny = unsigned((groups + wmax - 1) / wmax);
     const int nw = int((groups + ny - 1) / ny);
-    // fused when a tile spans at most 3 CTAs: measured faster there (config
-    // 3: 1 CTA, 190.3 -> 188.0 ms; config 1: 3 CTAs, 0.109 -> 0.104 ms;
-    // config 2: 2 CTAs, equal) and slower at 4 (config 5: 744 -> 756 ms,
-    // config 4: 5588 -> 5922 ms), where the per-CTA prologue (fp64 loads,
-    // the tile sort) repeated by every CTA of the tile and the last CTA's
-    // relax of N x 64 values outweigh the two launches saved
+    // sorted tiles are fused when a tile spans at most 3 CTAs: measured
+    // faster there (config 2: 2 CTAs, equal or better) and slower at 4
+    // (config 5: 744 -> 756 ms, config 4: 5588 -> 5922 ms), where the
+    // per-CTA prologue (fp64 loads, the O(N^2) tile sort) repeated by every
+    // CTA of the tile and the last CTA's relax of N x 64 values outweigh the
+    // two launches saved.  Unsorted tiles (N <= 24, no sort) are always
+    // fused (config 3: 1 CTA, 190.3 -> 188.0 ms; config 1: 5 CTAs, 0.102
+    // -> 0.093 ms)
     static const bool fuse_all = env_int("TURBDA_F32_FUSE_ALL", 0) != 0;
-    const bool fused = !global_x && !a.minibatch && !exact && !unfused && (ny <= 3 || fuse_all);
+    const bool fused =
+        !global_x && !a.minibatch && !exact && !unfused && (ny <= 3 || !sorted || fuse_all);
     // fused: + the sort staging columns, and room for the epilogue's
     // particles (nw P of them, which can exceed m by up to P - 1)
     const size_t smem =
@@ -1132,11 +1140,9 @@ cudaError_t launch_f32_p(const KernelArgs& a, float* xt, const double2* ab,
         add_launches(1);
         if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
     }
+    // fused over several CTAs: the tickets are zero (zeroed when the scratch
+    // is allocated, reset by each tile's last CTA)
     auto go = [&](auto kern) {
-        if (fused && ny > 1) {  // the last CTA of each tile resets its ticket
-            cudaError_t e = cudaMemsetAsync(a.tile_ticket, 0, sizeof(unsigned int) * tiles, st);
-            if (e != cudaSuccess) return e;
-        }
         cudaError_t e = launch_kernel(kern, grid, block, smem, st, a, xt, ab, steps, batches, z,
                                       status);
         add_launches(1);
@@ -1152,11 +1158,19 @@ cudaError_t launch_f32_p(const KernelArgs& a, float* xt, const double2* ab,
     if (a.minibatch) return go(ensf_f32_kernel<P, true, false, 0, 3>);
     if (!sorted) {
         if (exact) return go(ensf_f32_kernel<P, false, false, 0, 4, false, 256, false>);
-        static const int j20 = env_int("TURBDA_F32_J20", 0);
-        if (j20 && fused && a.j_batch == 20 && ((a.d_total | a.k0) & 1) == 0) {
-            if (j20 == 1) return go(ensf_f32_kernel<P, false, false, 0, 4, false, 256, true, true, true, 20>);
-            if (j20 == 2) return go(ensf_f32_kernel<P, false, false, 0, 3, false, 256, true, true, true, 20>);
-            if (j20 == 3) return go(ensf_f32_kernel<P, false, false, 0, 2, false, 256, true, true, true, 20>);
+        // grids under a wave with N = 20 (config 1): the member loop fully
+        // unrolled at compile time with the step's noise drawn inside the same
+        // basic block (ptxas interleaves the Philox / Box-Muller chain with the
+        // exponentials), 4-warp CTAs, no register cap that matters at this
+        // occupancy (with the 4-warp CTAs 0.102 -> 0.080 ms).  Same bits as the generic kernel
+        // (same accumulation order); TURBDA_F32_J20=0 disables.  The even-n0
+        // noise path needs even d_total and k0.
+        static const bool j20 = env_int("TURBDA_F32_J20", 1) != 0;
+        if constexpr (P == 1) {
+            if (j20 && fused && a.j_batch == 20 && ((a.d_total | a.k0) & 1) == 0) {
+                // 4-warp CTAs, 5 resident per SM (92 registers)
+                return go(ensf_f32_kernel<1, false, false, 0, 5, false, 128, true, true, true, 20>);
+            }
         }
         return fused ? go(ensf_f32_kernel<P, false, false, kPolyUnsorted, 4, false, 256, true, true>)
                      : go(ensf_f32_kernel<P, false, false, kPolyUnsorted, 4>);
@@ -1277,9 +1291,6 @@ cudaError_t launch_ensf_f32(const KernelArgs& a, const double2* ab, const StepF3
     // over (member, particle-in-warp), so one P for every window keeps
     // sharded results bit-identical to the whole-state call (tying the slot
     // to the member index instead measured 1.4-2.7 % slower, configs 2/4/5)
-    static const int force_p = env_int("TURBDA_F32_FORCE_P", 0);
-    if (!sorted && force_p == 1) return launch_f32_p<1>(a, xt, ab, steps, batches, z, status, st, sorted);
-    if (!sorted && force_p == 2) return launch_f32_p<2>(a, xt, ab, steps, batches, z, status, st, sorted);
     if (sorted || ((a.m % 4 == 0 || a.m >= 32) && warps_for(4) >= wave))
         return launch_f32_p<4>(a, xt, ab, steps, batches, z, status, st, sorted);
     if ((a.m % 2 == 0 || a.m >= 16) && warps_for(2) >= wave / 2)

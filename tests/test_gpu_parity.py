@@ -532,6 +532,35 @@ def test_fused_kernel_bit_identical_to_three_launches(capi, tmp_path, m, d, stri
     assert np.array_equal(fused, three)
 
 
+@pytest.mark.parametrize("d,k0,d_total", [(8192, 0, 8192), (3000, 1000, 8000), (700, 7300, 8000)])
+def test_small_grid_n20_kernel_bit_identical_to_generic(tmp_path, d, k0, d_total):
+    """Grids under a wave with N = 20 (config 1) run the kernel whose member
+    loop is unrolled at compile time and whose noise is drawn before it, in
+    4-warp CTAs; TURBDA_F32_J20=0 (a fresh process) runs the generic loop.
+    Same accumulation order, same Philox draws: identical bits, for whole
+    states and windows (k0 > 0, a ragged last tile)."""
+    import os
+    import subprocess
+    import sys
+    g = np.random.default_rng(11)
+    x = g.standard_normal((20, d)).astype(np.float32).astype(np.float64)
+    y = g.standard_normal(d)
+    np.save(tmp_path / "x.npy", x)
+    np.save(tmp_path / "y.npy", y)
+    code = ("import numpy as np, sys; from paper_2407_12168_b200 import capi; "
+            "p = sys.argv[1]; x, y = np.load(p + '/x.npy'), np.load(p + '/y.npy'); "
+            f"np.save(p + '/out.npy', capi.analyze_host(x, y, 0.8, None, n_steps=50, k0={k0}, "
+            f"d_total={d_total}))")
+    env = dict(os.environ, TURBDA_F32_J20="0")
+    subprocess.run([sys.executable, "-c", code, str(tmp_path)], check=True, env=env,
+                   cwd=str(Path(__file__).resolve().parents[1]))
+    generic = np.load(tmp_path / "out.npy")
+    from paper_2407_12168_b200 import capi
+    got = capi.analyze_host(x, y, 0.8, None, n_steps=50, k0=k0, d_total=d_total)
+    assert np.isfinite(got).all()
+    assert np.array_equal(got, generic)
+
+
 @pytest.mark.parametrize("m,d,stride", [(128, 2048 + 6, 3), (512, 640, 1), (200, 4700, 2)])
 def test_fused_kernel_at_many_ctas_per_tile_bit_identical(tmp_path, m, d, stride):
     """Tiles spread over 4-8 CTAs (N = 128, 512 with 32-warp CTAs, 200) run
