@@ -653,11 +653,34 @@ __global__ void __launch_bounds__(256, 2) joint_apply_tc_big_kernel(
 // N >= 128: the 128 x 128 tiles of gram_partial_big_kernel
 bool joint_gram_big(int n, int m) { return n >= kT2 && m >= kT2; }
 
+template <class K>
+cudaError_t resident_ctas(K kern, int threads, size_t smem, int64_t* out);
+
 JointPlan joint_plan(int n, int m, int64_t dl) {
     JointPlan pl;
-    const int tt = joint_gram_big(n, m) ? kT2 : kT;
+    const bool big = joint_gram_big(n, m);
+    const int tt = big ? kT2 : kT;
     const int tiles = ((n + tt - 1) / tt) * ((m + tt - 1) / tt);
-    pl.nchunk = (296 + tiles - 1) / tiles;  // ~2 CTAs per SM in total
+    // chunks x tiles CTAs in whole waves of the resident CTA slots: the big
+    // kernel (126 registers x 512 threads) fits one CTA per SM, and the
+    // round-1 rule (~296 CTAs) gave config 4 304 CTAs = 2 waves + 8 CTAs
+    // (26.4 ms per Gram; 592 CTAs = 4 full waves: 18.2 ms).  The 64 x 64
+    // kernel keeps ~296 CTAs, tuned at config 2's shape.
+    int64_t slots = 296;
+    if (big) resident_ctas(gram_partial_big_kernel, 512, 0, &slots);
+    slots = std::max<int64_t>(slots, 1);
+    int best = int((296 + tiles - 1) / tiles);
+    double best_eff = 0.0;
+    for (int waves = 1; big && waves <= 8; ++waves) {
+        const int64_t nc = std::max<int64_t>(waves * slots / tiles, 1);
+        const int64_t ctas = nc * tiles;
+        const double eff = double(ctas) / double((ctas + slots - 1) / slots * slots);
+        if (eff > best_eff + 0.01) {
+            best_eff = eff;
+            best = int(nc);
+        }
+    }
+    pl.nchunk = best;
     const int64_t want = (dl + pl.nchunk - 1) / pl.nchunk;
     pl.chunk = (want + kK - 1) / kK * kK;
     if (pl.chunk < kK) pl.chunk = kK;
