@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(256) joint_apply_tc_kernel(
 // chunks of 32: a W block [64 particles][32 members] and an X block
 // [32 members][64 coordinates] per stage, cp.async double-buffered over the
 // flattened (item, chunk) sequence.  W (N x N fp64) stays L2-resident.
-constexpr int kBigK = 32, kBigLdw = 36;
+constexpr int kBigK = 32, kBigLdw = 36, kBigStages = 2;  // 3 measured equal
 
 template <bool kF32Noise>
 __global__ void __launch_bounds__(256, 2) joint_apply_tc_big_kernel(
@@ -566,22 +566,36 @@ __global__ void __launch_bounds__(256, 2) joint_apply_tc_big_kernel(
     const int ngroups = (m + 63) / 64, nchunk = (m + kBigK - 1) / kBigK;
     const size_t wsz = size_t(64) * kBigLdw, xsz = size_t(kBigK) * kTcLdx;
     double* const W0 = jsm;                                  // [2][64][kBigLdw]
-    double* const X0 = W0 + 2 * wsz;                         // [2][kBigK][kTcLdx]
-    double2* const AB = reinterpret_cast<double2*>(X0 + 2 * xsz);  // [64] of the item's tile
+    double* const X0 = W0 + kBigStages * wsz;                // [kBigStages][kBigK][kTcLdx]
+    double2* const AB = reinterpret_cast<double2*>(X0 + kBigStages * xsz);  // [64] of the item's tile
     const int tid = threadIdx.x, nt = blockDim.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int lr = lane >> 2, lk = lane & 3;
     const bool aligned = (a.dl & 1) == 0;
     const int64_t nitems = ntiles * ngroups;
-    const int64_t my_items = (nitems - blockIdx.x + gridDim.x - 1) / gridDim.x;
-    const int64_t nseq = my_items * nchunk;
 
-    const auto issue = [&](int64_t sq, int b) {
-        const int64_t item = blockIdx.x + (sq / nchunk) * gridDim.x;
-        const int kc = int(sq % nchunk);
-        const int64_t tile = item / ngroups;
-        const int g = int(item % ngroups);
-        const int64_t k0 = tile * 64;
+    // stage = (item, member chunk kc); items blockIdx.x, + gridDim.x, ...
+    // advanced incrementally (no 64-bit divisions per stage: they were a
+    // third of the kernel's issue slots at config 4)
+    struct Stage {
+        int64_t item, tile;
+        int g, kc;
+    };
+    const auto advance = [&](Stage& t) {
+        if (++t.kc == nchunk) {
+            t.kc = 0;
+            t.item += gridDim.x;
+            t.g += int(gridDim.x % unsigned(ngroups));
+            t.tile += int64_t(gridDim.x / unsigned(ngroups));
+            if (t.g >= ngroups) {
+                t.g -= ngroups;
+                ++t.tile;
+            }
+        }
+    };
+    const auto issue = [&](const Stage& t, int b) {
+        const int kc = t.kc, g = t.g;
+        const int64_t k0 = t.tile * 64;
         double* Ws = W0 + b * wsz;
         double* Xs = X0 + b * xsz;
         for (int q = tid; q < 64 * (kBigK / 2); q += nt) {  // W block, 16 B per copy
@@ -612,22 +626,25 @@ __global__ void __launch_bounds__(256, 2) joint_apply_tc_big_kernel(
     };
 
     double acc[8][2];
-    if (nseq > 0) issue(0, 0);
-    for (int64_t sq = 0; sq < nseq; ++sq) {
-        const int b = int(sq & 1);
-        const int kc = int(sq % nchunk);
-        const int64_t item = blockIdx.x + (sq / nchunk) * gridDim.x;
-        const int64_t tile = item / ngroups;
-        const int g = int(item % ngroups);
-        const int64_t k0 = tile * 64;
+    Stage cur{int64_t(blockIdx.x), int64_t(blockIdx.x / unsigned(ngroups)),
+              int(blockIdx.x % unsigned(ngroups)), 0};
+    // double-buffered cp.async: stage i + 1 in flight while i feeds the
+    // tensor cores (a three-stage ring measured equal at config 4: 26.9 vs
+    // 26.5 ms per apply)
+    Stage s1 = cur;
+    advance(s1);
+    if (cur.item < nitems) issue(cur, 0);
+    for (int b = 0; cur.item < nitems; b ^= 1) {
+        const int kc = cur.kc, g = cur.g;
+        const int64_t k0 = cur.tile * 64;
         if (kc == 0) {
 #pragma unroll
             for (int n8 = 0; n8 < 8; ++n8) acc[n8][0] = acc[n8][1] = 0.0;
             for (int q = tid; q < 64; q += nt)
                 AB[q] = k0 + q < a.dl ? ab[k0 + q] : make_double2(0.0, 0.0);
         }
-        if (sq + 1 < nseq) {
-            issue(sq + 1, b ^ 1);  // released by the previous stage's barrier
+        if (s1.item < nitems) {
+            issue(s1, b ^ 1);  // released by the previous stage's barrier
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
@@ -645,6 +662,8 @@ __global__ void __launch_bounds__(256, 2) joint_apply_tc_big_kernel(
             joint_update_epilogue<kF32Noise>(a, c, step, 64 * g + 8 * warp + lr, k0, lk, acc, AB, z,
                                              status);
         __syncthreads();  // stage buffers (and AB) released
+        cur = s1;
+        advance(s1);
     }
 }
 
@@ -789,7 +808,7 @@ cudaError_t launch_joint_update(const KernelArgs& a, const double* x, const doub
         return cudaGetLastError();
     }
     if (tc_env) {
-        const size_t smem = sizeof(double) * (2 * size_t(64) * kBigLdw + 2 * size_t(kBigK) * kTcLdx) +
+        const size_t smem = sizeof(double) * kBigStages * (size_t(64) * kBigLdw + size_t(kBigK) * kTcLdx) +
                             sizeof(double2) * 64;
         auto kern = f32_noise ? joint_apply_tc_big_kernel<true> : joint_apply_tc_big_kernel<false>;
         int64_t resident = 0;
