@@ -400,7 +400,11 @@ __global__ void __launch_bounds__(kJW * 32, 2) joint_apply_kernel(
 // coordinate pair) — exactly the unit of the Euler-Maruyama update and of
 // one Philox block of particle noise — so the update runs in the epilogue.
 // Persistent CTAs keep W resident and stream X tiles; X is read once per step.
-constexpr int kTcLdx = 72;  // X tile row stride (doubles): conflict-free B loads
+// X tile row stride (doubles), = 4 mod 16: the B-fragment LDS.64 of a
+// half-warp (lk = 0..3 rows, lr = 0..3 columns) hit 16 distinct bank pairs.
+// 72 (= 8 mod 16) put rows lk and lk + 2 on the same banks: 2x the ideal
+// shared wavefronts (ncu, config 4 apply: 45 % of them excessive).
+constexpr int kTcLdx = 68;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
