@@ -430,7 +430,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) ensf_f32_kernel(KernelAr
                           &tile_bar);
         }
     }
-    // likelihood operator for this pair: B - A z with A = sum 1/r, B = sum y/r
+    // likelihood operator for this pair: B - A z with A = sum 1/r, B = sum y/r.
+    // Fused launches are programmatic dependents of the observation prep
+    // (the prologue above reads only the caller's forecast): wait for it
+    // here.  A no-op for ordinary launches.
+    if (kFused) asm volatile("griddepcontrol.wait;" ::: "memory");
     float2 A2 = f2(0.f), B2 = f2(0.f);
     if (kl < a.dl) {
         const double2 o = ab[kl];
@@ -881,6 +885,9 @@ __global__ void relax_kernel(const T* __restrict__ z, const double* __restrict__
 // r_stride 0: one error variance for every observation (TURBDA_R_UNIFORM)
 __global__ void obs_identity_kernel(const double* __restrict__ y, const double* __restrict__ r,
                                     int64_t r_stride, int64_t dl, double2* __restrict__ ab) {
+    // the fused analysis kernel may launch now (it waits for this grid's
+    // results with griddepcontrol.wait before reading {A, B})
+    asm volatile("griddepcontrol.launch_dependents;");
     const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k < dl) {
         const double inv = 1.0 / r[k * r_stride];
@@ -895,6 +902,9 @@ __global__ void obs_select_unique_kernel(const double* __restrict__ y, const dou
                                          int64_t r_stride, const int64_t* __restrict__ idx,
                                          int64_t obs_dim, int64_t k0, int64_t dl,
                                          double2* __restrict__ ab) {
+    // the fused analysis kernel may launch now (it waits for this grid's
+    // results with griddepcontrol.wait before reading {A, B})
+    asm volatile("griddepcontrol.launch_dependents;");
     const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (q >= obs_dim) return;
     const int64_t k = idx[q] - k0;
@@ -924,6 +934,9 @@ __global__ void obs_select_runs_kernel(const double* __restrict__ y, const doubl
                                        int64_t r_stride, const uint32_t* __restrict__ keys,
                                        const int32_t* __restrict__ pos, int64_t obs_dim,
                                        int64_t dl, double2* __restrict__ ab) {
+    // the fused analysis kernel may launch now (it waits for this grid's
+    // results with griddepcontrol.wait before reading {A, B})
+    asm volatile("griddepcontrol.launch_dependents;");
     const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= obs_dim) return;
     const uint32_t key = keys[t];
@@ -1051,14 +1064,31 @@ template <class K>
 cudaError_t launch_kernel(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                           const KernelArgs& a, const float* xt, const double2* ab,
                           const StepF32* steps, const int32_t* batches, float* z,
-                          unsigned long long* status) {
+                          unsigned long long* status, bool dependent = false) {
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              int(smem));
         if (e != cudaSuccess) return e;
     }
-    kern<<<grid, block, smem, st>>>(a, xt, ab, steps, batches, z, status);
-    return cudaGetLastError();
+    static const bool pdl = env_int("TURBDA_PDL", 1) != 0;
+    if (!(dependent && pdl)) {
+        kern<<<grid, block, smem, st>>>(a, xt, ab, steps, batches, z, status);
+        return cudaGetLastError();
+    }
+    // programmatic dependent launch: the grid is scheduled while the
+    // observation prep still runs, its prologue (forecast tile loads,
+    // conversion, statistics) overlaps that kernel and the launch latency
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a, xt, ab, steps, batches, z, status);
 }
 
 // Kernel choice (sweeps in profiles/):
@@ -1144,7 +1174,7 @@ cudaError_t launch_f32_p(const KernelArgs& a, float* xt, const double2* ab,
     // is allocated, reset by each tile's last CTA)
     auto go = [&](auto kern) {
         cudaError_t e = launch_kernel(kern, grid, block, smem, st, a, xt, ab, steps, batches, z,
-                                      status);
+                                      status, fused);
         add_launches(1);
         if (e != cudaSuccess || fused) return e;
         relax_kernel<float><<<blocks_for(a.dl, 256), 256, 0, st>>>(z, a.x64, a.m, a.dl, a.relax,
