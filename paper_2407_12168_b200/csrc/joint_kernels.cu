@@ -507,6 +507,7 @@ __global__ void __launch_bounds__(256) joint_apply_tc_kernel(
             const int j = q >> 5, l = q & 31;
             const int64_t k = k0 + 2 * l;
             double* dst = Xs + j * kTcLdx + 2 * l;
+            TB_CHECK(sizeof(double) * size_t(dst + 2 - jsm) <= dyn_smem_bytes());
             const double* row = x + size_t(j) * size_t(a.dl);
             if (j < m && aligned && k + 1 < a.dl) {
                 cp_async16(dst, row + k);
@@ -543,6 +544,8 @@ __global__ void __launch_bounds__(256) joint_apply_tc_kernel(
             for (int kq = 0; kq < mk; kq += 4) {
                 const double av = Ws[(8 * warp + lr) * ldw + kq + lk];
                 const double* xb = Xs + (kq + lk) * kTcLdx + lr;
+                TB_CHECK((8 * warp + lr) * ldw + kq + lk < mp8 * ldw);
+                TB_CHECK(sizeof(double) * size_t(xb + 57 - jsm) <= dyn_smem_bytes());
 #pragma unroll
                 for (int n8 = 0; n8 < 8; ++n8) dmma_8x8x4(acc[n8], av, xb[8 * n8]);
             }
@@ -606,6 +609,7 @@ __global__ void __launch_bounds__(256, 2) joint_apply_tc_big_kernel(
             const int r = q / (kBigK / 2), cc = 2 * (q % (kBigK / 2));
             const int gi = 64 * g + r, gj = kBigK * kc + cc;
             double* dst = Ws + r * kBigLdw + cc;
+            TB_CHECK(r < 64 && cc + 2 <= kBigLdw);
             if (gi < m && gj + 1 < m) {
                 cp_async16(dst, wn + size_t(gi) * m + gj);
             } else {
@@ -618,6 +622,7 @@ __global__ void __launch_bounds__(256, 2) joint_apply_tc_big_kernel(
             const int gj = kBigK * kc + j;
             const int64_t k = k0 + 2 * l;
             double* dst = Xs + j * kTcLdx + 2 * l;
+            TB_CHECK(sizeof(double) * size_t(dst + 2 - jsm) <= dyn_smem_bytes());
             const double* row = x + size_t(gj) * size_t(a.dl);
             if (gj < m && aligned && k + 1 < a.dl) {
                 cp_async16(dst, row + k);
@@ -659,6 +664,8 @@ __global__ void __launch_bounds__(256, 2) joint_apply_tc_big_kernel(
         for (int kq = 0; kq < kBigK; kq += 4) {
             const double av = Ws[(8 * warp + lr) * kBigLdw + kq + lk];
             const double* xb = Xs + (kq + lk) * kTcLdx + lr;
+            TB_CHECK(8 * warp + lr < 64 && kq + lk < kBigK);
+            TB_CHECK(sizeof(double) * size_t(xb + 57 - jsm) <= dyn_smem_bytes());
 #pragma unroll
             for (int n8 = 0; n8 < 8; ++n8) dmma_8x8x4(acc[n8], av, xb[8 * n8]);
         }
