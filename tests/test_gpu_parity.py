@@ -532,31 +532,40 @@ def test_fused_kernel_bit_identical_to_three_launches(capi, tmp_path, m, d, stri
     assert np.array_equal(fused, three)
 
 
-@pytest.mark.parametrize("d,k0,d_total", [(8192, 0, 8192), (3000, 1000, 8000), (700, 7300, 8000)])
-def test_small_grid_n20_kernel_bit_identical_to_generic(tmp_path, d, k0, d_total):
+@pytest.mark.parametrize("d,k0,d_total,stride,arctan", [(8192, 0, 8192, 0, False),
+                                                       (3000, 1000, 8000, 0, False),
+                                                       (700, 7300, 8000, 0, False),
+                                                       (2048, 0, 2048, 3, True)])
+def test_small_grid_n20_kernel_bit_identical_to_generic(tmp_path, d, k0, d_total, stride, arctan):
     """Grids under a wave with N = 20 (config 1) run the kernel whose member
     loop is unrolled at compile time and whose noise is drawn before it, in
     4-warp CTAs; TURBDA_F32_J20=0 (a fresh process) runs the generic loop.
     Same accumulation order, same Philox draws: identical bits, for whole
-    states and windows (k0 > 0, a ragged last tile)."""
+    states and windows (k0 > 0, a ragged last tile), and for the arctan
+    operator on a stride-3 selection."""
     import os
     import subprocess
     import sys
     g = np.random.default_rng(11)
     x = g.standard_normal((20, d)).astype(np.float32).astype(np.float64)
-    y = g.standard_normal(d)
+    idx = np.arange(0, d, stride, dtype=np.int64) if stride else None
+    y = g.standard_normal(d if idx is None else idx.size)
+    if arctan:
+        y = np.arctan(y)
     np.save(tmp_path / "x.npy", x)
     np.save(tmp_path / "y.npy", y)
+    np.save(tmp_path / "i.npy", idx if idx is not None else np.zeros(0, np.int64))
     code = ("import numpy as np, sys; from paper_2407_12168_b200 import capi; "
-            "p = sys.argv[1]; x, y = np.load(p + '/x.npy'), np.load(p + '/y.npy'); "
-            f"np.save(p + '/out.npy', capi.analyze_host(x, y, 0.8, None, n_steps=50, k0={k0}, "
-            f"d_total={d_total}))")
+            "p = sys.argv[1]; x, y, i = np.load(p + '/x.npy'), np.load(p + '/y.npy'), np.load(p + '/i.npy'); "
+            "i = i if i.size else None; "
+            f"np.save(p + '/out.npy', capi.analyze_host(x, y, 0.8, i, n_steps=50, k0={k0}, "
+            f"d_total={d_total}, arctan={arctan}))")
     env = dict(os.environ, TURBDA_F32_J20="0")
     subprocess.run([sys.executable, "-c", code, str(tmp_path)], check=True, env=env,
                    cwd=str(Path(__file__).resolve().parents[1]))
     generic = np.load(tmp_path / "out.npy")
     from paper_2407_12168_b200 import capi
-    got = capi.analyze_host(x, y, 0.8, None, n_steps=50, k0=k0, d_total=d_total)
+    got = capi.analyze_host(x, y, 0.8, idx, n_steps=50, k0=k0, d_total=d_total, arctan=arctan)
     assert np.isfinite(got).all()
     assert np.array_equal(got, generic)
 
