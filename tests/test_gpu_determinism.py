@@ -197,3 +197,27 @@ def test_likelihood_score_and_sde_step_on_device(capi):
     assert L.turbda_reverse_sde_step(zz.ctypes.data, n, d, t, dt, sc.ctypes.data, xi.ctypes.data, 0,
                                      C.byref(st)) == capi.DIVERGED
     assert st.diverged_t == t
+
+
+@pytest.mark.parametrize("precision,tol", [(1, FP64_TOL), (0, FP32_TOL)])
+@pytest.mark.parametrize("m,d", [(20, 8192), (64, 3000)])
+def test_selection_without_observations_in_the_window(capi, port, precision, tol, m, d):
+    """A selection operator whose window holds no observation (obs_dim = 0,
+    or every index outside [k0, k0 + d)): the prep leaves {A, B} = 0 through
+    a memset alone, so the fused kernel (a programmatic dependent launch)
+    follows a memset, not a kernel; the analysis is the prior-only sampler."""
+    x, _, _, _ = conditioned_inputs(m, d)
+    x = x.astype(np.float32).astype(np.float64)
+    want = port.analyze(x, np.zeros(0), 1.0, np.zeros(0, np.int64), n_steps=20)
+    got = capi.analyze_host(x, np.zeros(0), 1.0, np.zeros(0, np.int64), n_steps=20,
+                            precision=precision)
+    assert np.isfinite(got).all()
+    assert rel_l2(got, want) <= tol
+    # the same state as the window [d, 2d) of a 2d state whose observations all
+    # sit in the other half
+    idx = np.arange(0, d, 7, dtype=np.int64)
+    y = np.ones(idx.size)
+    got_w = capi.analyze_host(x, y, 1.0, idx, n_steps=20, k0=d, d_total=2 * d,
+                              precision=precision)
+    want_w = port.analyze(x, y[:0], 1.0, idx[:0], n_steps=20, k0=d, d_total=2 * d)
+    assert rel_l2(got_w, want_w) <= tol
