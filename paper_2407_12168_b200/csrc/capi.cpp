@@ -207,7 +207,7 @@ struct Workspace {
     void* jsym = nullptr;                       // symmetric-window joint buffer
     void* jsym_win = nullptr;
     size_t jsym_bytes = 0;
-    DevBuf jpart, jred, jw;                     // joint-mode scratch
+    DevBuf jpart, jred, jw, jxbar;              // joint-mode scratch
     cudaGraphExec_t jgraph = nullptr;           // joint mode: captured pseudo-steps
     std::vector<cudaStream_t> cstreams;         // host-mode chunk pipeline
     std::vector<cudaEvent_t> ev_chunk;
@@ -987,6 +987,12 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
         red = w->jred.as<double>();
     }
     TB_CUDA(w->jw.reserve(sizeof(double) * size_t(m) * size_t(m)));
+    // N > 64: the weighted prior sums W X go through HBM ([N][d] fp64)
+    double* jxbar = nullptr;
+    if (m > 64) {
+        TB_CUDA(w->jxbar.reserve(sizeof(double) * md));
+        jxbar = w->jxbar.as<double>();
+    }
     TB_CUDA(w->status.reserve(64));
     unsigned long long* dstatus = w->status.as<unsigned long long>();
     TB_CUDA(cudaMemsetAsync(dstatus, 0xff, sizeof(unsigned long long), s));
@@ -1056,7 +1062,7 @@ int run_joint(const turbda_ensf_params* p, const Window& win, int device, const 
         }
         if (ge == cudaSuccess)
             ge = launch_joint_update(a, dx, w->ab.as<double2>(), red, w->jw.as<double>(), c, step, z,
-                                     dstatus, p->precision == TURBDA_FP32, s);
+                                     dstatus, p->precision == TURBDA_FP32, s, jxbar);
         if (ge != cudaSuccess) {
             if (use_graph) {
                 cudaGraph_t g = nullptr;

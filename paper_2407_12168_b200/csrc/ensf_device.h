@@ -141,12 +141,12 @@ cudaError_t launch_joint_init(const KernelArgs& a, double* z, cudaStream_t st);
 // buffer a multi-GPU run allreduces)
 cudaError_t launch_joint_gram(const KernelArgs& a, const JointPlan& pl, const double* z,
                               const double* x, double* part, double* red, cudaStream_t st);
-// wn: m * m doubles of scratch
+// wn: m * m doubles of scratch; xbar: m * dl doubles of scratch (m > 64)
 // f32_noise: particle normals from the fp32 Box-Muller (TURBDA_FP32)
 cudaError_t launch_joint_update(const KernelArgs& a, const double* x, const double2* ab,
                                 const double* red, double* wn, const StepF64& c, int step,
                                 double* z, unsigned long long* status, bool f32_noise,
-                                cudaStream_t st);
+                                cudaStream_t st, double* xbar = nullptr);
 
 // rmse / spread sums in a fixed order: out[0] = sum (mean - truth)^2,
 // out[1] = sum dev^2; `out` holds diag_scratch_doubles() doubles (the

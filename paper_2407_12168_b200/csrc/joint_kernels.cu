@@ -419,19 +419,19 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // k0 + 8 n8 + 2 lk): score, damped likelihood, particle noise, Euler-
 // Maruyama, divergence check.  The particle's z pairs are loaded up front so
 // their latencies overlap.
-template <bool kF32Noise>
+template <bool kF32Noise, int NB = 8>
 __device__ __forceinline__ void joint_update_epilogue(const KernelArgs& a, const StepF64& c,
                                                       int step, int i, int64_t k0, int lk,
-                                                      const double (&acc)[8][2],
+                                                      const double (&acc)[NB][2],
                                                       const double2* abs, double* z,
                                                       unsigned long long* status) {
     if (i >= a.m) return;
     const bool aligned = (a.dl & 1) == 0;
     const double ib2 = 2.0 * c.inv2b;
     double* zrow = z + size_t(i) * size_t(a.dl);
-    double2 zp[8];
+    double2 zp[NB];
 #pragma unroll
-    for (int n8 = 0; n8 < 8; ++n8) {
+    for (int n8 = 0; n8 < NB; ++n8) {
         const int64_t kl = k0 + 8 * n8 + 2 * lk;
         zp[n8] = make_double2(0.0, 0.0);
         if (aligned && kl + 1 < a.dl)
@@ -440,7 +440,7 @@ __device__ __forceinline__ void joint_update_epilogue(const KernelArgs& a, const
             zp[n8] = make_double2(zrow[kl], kl + 1 < a.dl ? zrow[kl + 1] : 0.0);
     }
 #pragma unroll
-    for (int n8 = 0; n8 < 8; ++n8) {
+    for (int n8 = 0; n8 < NB; ++n8) {
         const int64_t kl = k0 + 8 * n8 + 2 * lk;
         if (kl >= a.dl) continue;
         const bool has_y = kl + 1 < a.dl;
@@ -555,127 +555,122 @@ __global__ void __launch_bounds__(256) joint_apply_tc_kernel(
     }
 }
 
-// N > 64: the same tensor-core update with the GEMM's K (members) and the
-// particles tiled.  Work item = (64-coordinate tile, group of 64 particles),
-// consecutive items share the member tile; per item the members stream in
-// chunks of 32: a W block [64 particles][32 members] and an X block
-// [32 members][64 coordinates] per stage, cp.async double-buffered over the
-// flattened (item, chunk) sequence.  W (N x N fp64) stays L2-resident.
-constexpr int kBigK = 32, kBigLdw = 36, kBigStages = 2;  // 3 measured equal
+// N > 64: the weighted prior sums xbar = W X as one GEMM (M = N particles,
+// N = the coordinates, K = the members) in 128 x 128 tiles of 16 warps, each
+// a 16 x 64 block of 2 x 8 DMMA tiles (the Gram kernel's shape), written to
+// HBM; then an elementwise update.  Config 4 (N = 512): GEMM 17.9 ms + update
+// 3.5 ms per pseudo-step against 25.7 ms for a fused apply (64 x 64 tiles with
+// the update in the epilogue, whose tensor pipe stayed ~55 % busy), for 8.6
+// GB more HBM traffic.  The K order (members 0, 4, 8, ... in DMMA groups of
+// 4) is the fused kernel's, so the bits are the same.
+constexpr int kWxK = 16, kWxLdw = 20, kWxLdx = 132;  // row strides = 4 mod 16
 
-template <bool kF32Noise>
-__global__ void __launch_bounds__(256, 2) joint_apply_tc_big_kernel(
-    KernelArgs a, const double* __restrict__ x, const double2* __restrict__ ab,
-    const double* __restrict__ wn, StepF64 c, int step, double* __restrict__ z,
-    unsigned long long* __restrict__ status, int64_t ntiles) {
-    extern __shared__ double jsm[];
-    const int m = a.m;
-    const int ngroups = (m + 63) / 64, nchunk = (m + kBigK - 1) / kBigK;
-    const size_t wsz = size_t(64) * kBigLdw, xsz = size_t(kBigK) * kTcLdx;
-    double* const W0 = jsm;                                  // [2][64][kBigLdw]
-    double* const X0 = W0 + kBigStages * wsz;                // [kBigStages][kBigK][kTcLdx]
-    double2* const AB = reinterpret_cast<double2*>(X0 + kBigStages * xsz);  // [64] of the item's tile
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int lane = tid & 31, warp = tid >> 5;
+__global__ void __launch_bounds__(512) joint_wx_gemm_kernel(const double* __restrict__ wn,
+                                                            const double* __restrict__ x, int m,
+                                                            int64_t dl, double* __restrict__ xbar) {
+    extern __shared__ double wxsm[];
+    auto ws = reinterpret_cast<double (*)[128][kWxLdw]>(wxsm);                      // [2][128][kWxLdw]
+    auto xs = reinterpret_cast<double (*)[kWxK][kWxLdx]>(wxsm + 2 * 128 * kWxLdw);   // [2][kWxK][kWxLdx]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int lr = lane >> 2, lk = lane & 3;
-    const bool aligned = (a.dl & 1) == 0;
-    const int64_t nitems = ntiles * ngroups;
-
-    // stage = (item, member chunk kc); items blockIdx.x, + gridDim.x, ...
-    // advanced incrementally (no 64-bit divisions per stage: they were a
-    // third of the kernel's issue slots at config 4)
-    struct Stage {
-        int64_t item, tile;
-        int g, kc;
-    };
-    const auto advance = [&](Stage& t) {
-        if (++t.kc == nchunk) {
-            t.kc = 0;
-            t.item += gridDim.x;
-            t.g += int(gridDim.x % unsigned(ngroups));
-            t.tile += int64_t(gridDim.x / unsigned(ngroups));
-            if (t.g >= ngroups) {
-                t.g -= ngroups;
-                ++t.tile;
-            }
-        }
-    };
-    const auto issue = [&](const Stage& t, int b) {
-        const int kc = t.kc, g = t.g;
-        const int64_t k0 = t.tile * 64;
-        double* Ws = W0 + b * wsz;
-        double* Xs = X0 + b * xsz;
-        for (int q = tid; q < 64 * (kBigK / 2); q += nt) {  // W block, 16 B per copy
-            const int r = q / (kBigK / 2), cc = 2 * (q % (kBigK / 2));
-            const int gi = 64 * g + r, gj = kBigK * kc + cc;
-            double* dst = Ws + r * kBigLdw + cc;
-            TB_CHECK(r < 64 && cc + 2 <= kBigLdw);
-            if (gi < m && gj + 1 < m) {
-                cp_async16(dst, wn + size_t(gi) * m + gj);
-            } else {
-                dst[0] = (gi < m && gj < m) ? wn[size_t(gi) * m + gj] : 0.0;
-                dst[1] = 0.0;
-            }
-        }
-        for (int q = tid; q < kBigK * 32; q += nt) {  // X block, 16 B per copy
-            const int j = q >> 5, l = q & 31;
-            const int gj = kBigK * kc + j;
-            const int64_t k = k0 + 2 * l;
-            double* dst = Xs + j * kTcLdx + 2 * l;
-            TB_CHECK(sizeof(double) * size_t(dst + 2 - jsm) <= dyn_smem_bytes());
-            const double* row = x + size_t(gj) * size_t(a.dl);
-            if (gj < m && aligned && k + 1 < a.dl) {
-                cp_async16(dst, row + k);
-            } else {
-                dst[0] = (gj < m && k < a.dl) ? __ldg(row + k) : 0.0;
-                dst[1] = (gj < m && k + 1 < a.dl) ? __ldg(row + k + 1) : 0.0;
-            }
-        }
-        cp_async_commit();
-    };
-
-    double acc[8][2];
-    Stage cur{int64_t(blockIdx.x), int64_t(blockIdx.x / unsigned(ngroups)),
-              int(blockIdx.x % unsigned(ngroups)), 0};
-    // double-buffered cp.async: stage i + 1 in flight while i feeds the
-    // tensor cores (a three-stage ring measured equal at config 4: 26.9 vs
-    // 26.5 ms per apply)
-    Stage s1 = cur;
-    advance(s1);
-    if (cur.item < nitems) issue(cur, 0);
-    for (int b = 0; cur.item < nitems; b ^= 1) {
-        const int kc = cur.kc, g = cur.g;
-        const int64_t k0 = cur.tile * 64;
-        if (kc == 0) {
+    const int wr = 16 * (warp >> 1), wc = 64 * (warp & 1);
+    const int nti = (m + 127) / 128;
+    const int64_t ntc = (dl + 127) / 128;
+    const int64_t ntiles = ntc * nti;
+    const int nks = (m + kWxK - 1) / kWxK;
+    const bool aligned = (dl & 1) == 0;
+    // staging: W block [128][16] as 2 x 4 doubles per thread, X block
+    // [16][128] as 2 x 2 x 2 doubles per thread
+    const int wrow = threadIdx.x >> 2, wcol = 4 * (threadIdx.x & 3);   // 128 rows x 4 quads
+    const int xrow = threadIdx.x >> 5, xcol = 4 * (threadIdx.x & 31);  // 16 rows x 32 quads
+    double wv[4], xv[4];
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int ti0 = int(t % nti) * 128;
+        const int64_t tc0 = (t / nti) * 128;
+        const auto fetch = [&](int ks) {
+            const int j0 = ks * kWxK;
+            const int gi = ti0 + wrow;
 #pragma unroll
-            for (int n8 = 0; n8 < 8; ++n8) acc[n8][0] = acc[n8][1] = 0.0;
-            for (int q = tid; q < 64; q += nt)
-                AB[q] = k0 + q < a.dl ? ab[k0 + q] : make_double2(0.0, 0.0);
-        }
-        if (s1.item < nitems) {
-            issue(s1, b ^ 1);  // released by the previous stage's barrier
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
+            for (int u = 0; u < 4; ++u) {
+                const int gj = j0 + wcol + u;
+                wv[u] = (gi < m && gj < m) ? __ldg(wn + size_t(gi) * m + gj) : 0.0;
+            }
+            const int gj = j0 + xrow;
+            const int64_t k = tc0 + xcol;
+            const double* row = x + size_t(gj) * size_t(dl);
+            if (gj < m && aligned && k + 3 < dl) {
+                const double2 a = __ldg(reinterpret_cast<const double2*>(row + k));
+                const double2 b = __ldg(reinterpret_cast<const double2*>(row + k + 2));
+                xv[0] = a.x; xv[1] = a.y; xv[2] = b.x; xv[3] = b.y;
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) xv[u] = (gj < m && k + u < dl) ? __ldg(row + k + u) : 0.0;
+            }
+        };
+        double acc[2][8][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) acc[h][nt][0] = acc[h][nt][1] = 0.0;
+        fetch(0);
+        for (int ks = 0; ks < nks; ++ks) {
+            const int b = ks & 1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                ws[b][wrow][wcol + u] = wv[u];
+                xs[b][xrow][xcol + u] = xv[u];
+            }
+            __syncthreads();
+            if (ks + 1 < nks) fetch(ks + 1);
+#pragma unroll
+            for (int kq = 0; kq < kWxK; kq += 4) {
+                const double a0 = ws[b][wr + lr][kq + lk];
+                const double a1 = ws[b][wr + 8 + lr][kq + lk];
+#pragma unroll
+                for (int nt = 0; nt < 8; ++nt) {
+                    const double bb = xs[b][kq + lk][wc + 8 * nt + lr];
+                    dmma_8x8x4(acc[0][nt], a0, bb);
+                    dmma_8x8x4(acc[1][nt], a1, bb);
+                }
+            }
+            // two buffers: the next stage writes the other one, and the
+            // barrier above orders this stage's reads before its overwrite
         }
         __syncthreads();
-        const double* Ws = W0 + b * wsz;
-        const double* Xs = X0 + b * xsz;
-        for (int kq = 0; kq < kBigK; kq += 4) {
-            const double av = Ws[(8 * warp + lr) * kBigLdw + kq + lk];
-            const double* xb = Xs + (kq + lk) * kTcLdx + lr;
-            TB_CHECK(8 * warp + lr < 64 && kq + lk < kBigK);
-            TB_CHECK(sizeof(double) * size_t(xb + 57 - jsm) <= dyn_smem_bytes());
 #pragma unroll
-            for (int n8 = 0; n8 < 8; ++n8) dmma_8x8x4(acc[n8], av, xb[8 * n8]);
+        for (int h = 0; h < 2; ++h) {
+            const int i = ti0 + wr + 8 * h + lr;
+            if (i >= m) continue;
+            double* orow = xbar + size_t(i) * size_t(dl);
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+                const int64_t k = tc0 + wc + 8 * nt + 2 * lk;
+                if (aligned && k + 1 < dl) {
+                    *reinterpret_cast<double2*>(orow + k) = make_double2(acc[h][nt][0], acc[h][nt][1]);
+                } else {
+                    if (k < dl) orow[k] = acc[h][nt][0];
+                    if (k + 1 < dl) orow[k + 1] = acc[h][nt][1];
+                }
+            }
         }
-        if (kc == nchunk - 1)
-            joint_update_epilogue<kF32Noise>(a, c, step, 64 * g + 8 * warp + lr, k0, lk, acc, AB, z,
-                                             status);
-        __syncthreads();  // stage buffers (and AB) released
-        cur = s1;
-        advance(s1);
     }
+}
+
+// Euler-Maruyama update from xbar: one thread per (particle, coordinate pair)
+template <bool kF32Noise>
+__global__ void __launch_bounds__(256) joint_update_xbar_kernel(KernelArgs a, const double* __restrict__ xbar,
+                                                                const double2* __restrict__ ab, StepF64 c,
+                                                                int step, double* __restrict__ z,
+                                                                unsigned long long* __restrict__ status) {
+    const int64_t pr = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int i = blockIdx.y;
+    const int64_t kl = 2 * pr;
+    if (kl >= a.dl) return;
+    const double* xr = xbar + size_t(i) * size_t(a.dl);
+    double acc[1][2];
+    acc[0][0] = xr[kl];
+    acc[0][1] = kl + 1 < a.dl ? xr[kl + 1] : 0.0;
+    joint_update_epilogue<kF32Noise, 1>(a, c, step, i, kl, 0, acc, ab + kl, z, status);
 }
 
 }  // namespace
@@ -796,7 +791,7 @@ cudaError_t resident_ctas(K kern, int threads, size_t smem, int64_t* out) {
 cudaError_t launch_joint_update(const KernelArgs& a, const double* x, const double2* ab,
                                 const double* red, double* wn, const StepF64& c, int step,
                                 double* z, unsigned long long* status, bool f32_noise,
-                                cudaStream_t st) {
+                                cudaStream_t st, double* xbar) {
     joint_softmax_kernel<<<unsigned((a.m + 3) / 4), 128, 0, st>>>(red, a.m, a.m, c.alpha, c.inv2b,
                                                                   wn);
     cudaError_t e = cudaGetLastError();
@@ -819,16 +814,21 @@ cudaError_t launch_joint_update(const KernelArgs& a, const double* x, const doub
         return cudaGetLastError();
     }
     if (tc_env) {
-        const size_t smem = sizeof(double) * kBigStages * (size_t(64) * kBigLdw + size_t(kBigK) * kTcLdx) +
-                            sizeof(double2) * 64;
-        auto kern = f32_noise ? joint_apply_tc_big_kernel<true> : joint_apply_tc_big_kernel<false>;
+        if (!xbar) return cudaErrorInvalidValue;
         int64_t resident = 0;
-        e = resident_ctas(kern, 256, smem, &resident);
+        const size_t wx_smem = sizeof(double) * 2 * (128 * kWxLdw + kWxK * kWxLdx);
+        e = resident_ctas(joint_wx_gemm_kernel, 512, wx_smem, &resident);
         if (e != cudaSuccess) return e;
-        const int64_t ntiles = (a.dl + 63) / 64;
-        const int64_t items = ntiles * ((a.m + 63) / 64);
-        const int64_t grid = std::min<int64_t>(items, resident);
-        kern<<<unsigned(grid), 256, smem, st>>>(a, x, ab, wn, c, step, z, status, ntiles);
+        const int64_t tiles = ((a.dl + 127) / 128) * ((a.m + 127) / 128);
+        joint_wx_gemm_kernel<<<unsigned(std::min<int64_t>(tiles, resident)), 512, wx_smem, st>>>(
+            wn, x, a.m, a.dl, xbar);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        const dim3 grid(unsigned((a.dl / 2 + 255) / 256 + 1), unsigned(a.m));
+        if (f32_noise)
+            joint_update_xbar_kernel<true><<<grid, 256, 0, st>>>(a, xbar, ab, c, step, z, status);
+        else
+            joint_update_xbar_kernel<false><<<grid, 256, 0, st>>>(a, xbar, ab, c, step, z, status);
         return cudaGetLastError();
     }
     const dim3 grid(unsigned((a.dl + 63) / 64), unsigned((a.m + kJP * kJW - 1) / (kJP * kJW)));
