@@ -474,6 +474,7 @@ def test_joint_mode_multi_process_nccl(capi):
     assert "JOINT_MULTIPROC_OK" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
     assert "SHARD_VERDICT_OK" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
     assert "EMPTY_WINDOW_OK" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "JOINT_BIG_MULTIPROC_OK" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
 
 
 def test_async_calls_on_two_streams_do_not_share_scratch(capi):

@@ -57,6 +57,21 @@ def main():
               f"{np.array_equal(got_c, whole_c)}", flush=True)
         ok = ej <= 1e-9 and np.array_equal(got_c, whole_c)
         print("JOINT_MULTIPROC_OK" if ok else "JOINT_MULTIPROC_FAIL", flush=True)
+    # N > 64 (the W X GEMM + elementwise update path), sharded
+    m2, d2 = 80, 3000
+    x2, y2, _, _ = conditioned_inputs(m2, d2)
+    x2 = 0.05 * x2
+    lo2, hi2 = d2 * rank // world, d2 * (rank + 1) // world
+    part_b = capi.analyze_host(x2[:, lo2:hi2], y2[lo2:hi2], 4.0, None, n_steps=20, joint=True,
+                               device=local, k0=lo2, d_total=d2, precision=capi.FP64, sharded=True)
+    parts_b = [None] * world
+    dist.all_gather_object(parts_b, (lo2, part_b))
+    if rank == 0:
+        parts_b.sort(key=lambda t: t[0])
+        got_b = np.concatenate([p[1] for p in parts_b], axis=1)
+        eb = rel_l2(got_b, PortOracle().analyze(x2, y2, 4.0, None, n_steps=20, joint=True))
+        print(f"joint N={m2} sharded x{world} vs oracle rel-L2 {eb:.3e}", flush=True)
+        print("JOINT_BIG_MULTIPROC_OK" if eb <= 1e-9 else "JOINT_BIG_MULTIPROC_FAIL", flush=True)
     # divergence only inside the last rank's window: every rank must report
     # the unsharded run's (particle, step)
     r = np.ones(d)
