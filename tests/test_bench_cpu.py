@@ -28,3 +28,22 @@ def test_bench_rejects_short_warmup():
     out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
                           "--warmup", "1"], capture_output=True, text=True, timeout=300)
     assert out.returncode != 0 and "warmup" in out.stderr
+
+
+def test_reference_arm_under_torchrun_world2():
+    """The driver launches the reference arm like its own (torchrun for
+    N > 1): rank 0 alone runs the reference and prints one line, the other
+    rank exits 0 without work."""
+    from oracle.oracle import ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                          "--master-port", "29611", str(ROOT / "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--steps", "1", "--warmup", "3", "--ref-sample-d", "640"],
+                         capture_output=True, text=True, timeout=600, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
