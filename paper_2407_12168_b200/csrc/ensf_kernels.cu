@@ -728,6 +728,10 @@ __global__ void __launch_bounds__(128) ensf_f64_kernel(KernelArgs a, const doubl
     __syncthreads();
 
     const int i0 = (blockIdx.y * nwarps + warp) * P;
+    // warps past the last particle (N = 20 at P = 2: 10 groups in 3 CTAs of
+    // 4 warps) leave instead of integrating padding particles; no barrier
+    // follows
+    if (i0 >= a.m) return;
     const uint64_t kg = uint64_t(a.k0 + kl);
 
     double zx[P], zy[P];
