@@ -221,3 +221,21 @@ def test_selection_without_observations_in_the_window(capi, port, precision, tol
                               precision=precision)
     want_w = port.analyze(x, y[:0], 1.0, idx[:0], n_steps=20, k0=d, d_total=2 * d)
     assert rel_l2(got_w, want_w) <= tol
+
+
+@pytest.mark.parametrize("m", [9, 21, 23, 41])
+def test_fp64_padding_warps_exit(capi, port, m):
+    """The fp64 kernel runs P = 2 particles per warp in 4-warp CTAs; warps
+    past the last particle leave before integrating (N = 21: 11 groups, the
+    third CTA has one padding warp; odd N: the last warp's second particle is
+    padding).  Parity with the C restatement and the lowest-particle
+    divergence verdict are unaffected."""
+    x, y, _, _ = conditioned_inputs(m, 1000)
+    got = capi.analyze_host(x, y, 1.0, None, n_steps=20, precision=capi.FP64)
+    want = port.analyze(x, y, 1.0, None, n_steps=20)
+    assert rel_l2(got, want) <= FP64_TOL
+    r = np.ones(1000)
+    r[3] = 1e-300  # diverges in every particle: the verdict names particle 0
+    with pytest.raises(capi.TurbdaError) as ei:
+        capi.analyze_host(x, y, r, None, n_steps=20, precision=capi.FP64)
+    assert ei.value.code == capi.DIVERGED and ei.value.diverged_particle == 0
